@@ -1,0 +1,183 @@
+/* fqg.h — C ABI of the B200 (sm_100a) FlattenQuant linear-layer hot path.
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (/root/reference/proj/core/include/fq/{flatten,quantize,pipeline}.hpp, namespace fq). Every entry point
+ * names the reference interface it replaces. Plain pointers and sizes only;
+ * device pointers are marked *_dev, streams are cudaStream_t passed as void*.
+ *
+ * Errors: every function returns an fqg_status. The message of the last
+ * failure on the calling thread is in fqg_last_error(). The C++ shim
+ * (include/fq_gpu.hpp) maps FQG_ERR_INVALID -> std::invalid_argument and
+ * FQG_ERR_RUNTIME -> std::runtime_error, the exception types the reference
+ * throws for the same conditions (pipeline.cpp:161-163, flatten.cpp:92-94,
+ * quantize.cpp:37). There is no CPU fallback: without a usable sm_100 device
+ * every compute entry point fails with FQG_ERR_CUDA.
+ *
+ * Layer handles are immutable after creation; fqg_layer_forward is
+ * stream-ordered and may be called concurrently on different streams.
+ */
+#ifndef FQG_H
+#define FQG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fqg_status {
+    FQG_OK = 0,
+    FQG_ERR_INVALID = -2,     /* std::invalid_argument in the reference */
+    FQG_ERR_RUNTIME = -3,     /* std::runtime_error in the reference   */
+    FQG_ERR_CUDA = -4,        /* CUDA / device failure (no fallback)   */
+    FQG_ERR_UNSUPPORTED = -5  /* shape/format outside this build       */
+} fqg_status;
+
+typedef enum fqg_dtype {
+    FQG_F64 = 0,
+    FQG_F32 = 1,
+    FQG_F16 = 2,
+    FQG_BF16 = 3,
+    FQG_I32 = 4, /* raw INT32 accumulators (bit-exact debug dump)          */
+    FQG_I8 = 5,  /* int8 operand, one value per byte                       */
+    FQG_I4 = 6,  /* packed int4 operand: byte b = q[2b] & 15 | q[2b+1] << 4 */
+    FQG_NONE = 7
+} fqg_dtype;
+
+/* Activation-scale mode. STATIC is the reference inference path
+ * (act_scale = T_x / qmax, pipeline.cpp:138,167). DYNAMIC is the opt-in
+ * per-tensor absmax mode whose oracle is quantize_per_tensor without an
+ * override (quantize.cpp:34-40), computed per call on the device. */
+typedef enum fqg_scale_mode { FQG_SCALE_STATIC = 0, FQG_SCALE_DYNAMIC = 1 } fqg_scale_mode;
+
+typedef struct fqg_layer_s* fqg_layer_t;
+
+/* The frozen recipe of one linear layer: the fields of fq::LayerQuantConfig
+ * (pipeline.hpp:37-49) that fq::run_layer reads, as plain arrays. */
+typedef struct fqg_layer_desc {
+    int bits;                     /* 4 or 8 (LayerQuantConfig::bits)              */
+    int64_t k;                    /* input channels K                              */
+    int64_t n;                    /* output channels of THIS shard                 */
+    const double* smooth_scales;  /* [k] host, SmoothingScales::s                  */
+    double t_x;                   /* plan_x.threshold                              */
+    const int64_t* ext_x;         /* [k] host, plan_x.extensions                   */
+    int64_t block_x;              /* plan_x.block (32)                             */
+    double t_w;                   /* plan_w.threshold                              */
+    const int64_t* ext_w;         /* [plan_x.padded_width] host, plan_w.extensions */
+    int64_t block_w;              /* plan_w.block                                  */
+    double act_scale;             /* LayerQuantConfig::act_scale (static s_x)      */
+    /* Weights, one of:
+     *  (a) weight_q != NULL: reference weight_q.q, int32 [K'][n_total] row-major
+     *      (host), with w_scale = weight_q.params.scale;
+     *  (b) weight != NULL: the unquantized layer weight W, f64 [k][n_total]
+     *      row-major (host). The offline tail of quantize_layer
+     *      (pipeline.cpp:100,114-120,139-150) runs on the device: scale_rows,
+     *      repeat_channels, strict flatten_rows, per-tensor absmax -> s_w,
+     *      round-to-nearest quantization; w_scale is ignored (computed). */
+    const int32_t* weight_q;
+    const double* weight;
+    double w_scale;
+    int64_t n_total;              /* columns of the full layer (== n unsharded)    */
+    int64_t n_begin;              /* first column of this shard                    */
+    int a_format;                 /* FQG_I8, or FQG_I4 (packed activations; bits=4) */
+    int b_format;                 /* FQG_I8, or FQG_I4 (packed weights; bits=4)    */
+    int scale_mode;               /* fqg_scale_mode                                */
+    int device;                   /* CUDA device ordinal                           */
+} fqg_layer_desc;
+
+typedef struct fqg_layer_info {
+    int bits, a_format, b_format, scale_mode;
+    int64_t k, n, c1, kp, n_total, n_begin;
+    double t_x, t_w, act_scale, w_scale;
+    int64_t weight_bytes;         /* device bytes of the packed weight operand     */
+} fqg_layer_info;
+
+const char* fqg_last_error(void);
+int fqg_version(void);
+
+/* Replaces the construction of a runnable LayerQuantConfig (cmd_infer's
+ * load_recipes, flattenquant_cli.cpp:241-252, and the weight tail of
+ * fq::quantize_layer, pipeline.cpp:100,114-120,139-150): compiles the
+ * composite gather map from plan_x/plan_w, quantizes/packs the weights
+ * K-major on the device, uploads the per-channel tables. */
+int fqg_layer_create(const fqg_layer_desc* desc, fqg_layer_t* out);
+int fqg_layer_destroy(fqg_layer_t layer);
+int fqg_layer_get_info(fqg_layer_t layer, fqg_layer_info* info);
+/* Device copy of the quantized weight (int32 [K'][n] row-major, the
+ * reference's weight_q layout for this shard) and s_w, for parity checks. */
+int fqg_layer_weight_q(fqg_layer_t layer, int32_t* wq_host, double* w_scale);
+
+/* Replaces fq::run_layer (pipeline.hpp:83-84, pipeline.cpp:159-169) on
+ * device-resident data: y = dequant(int_gemm(quant(repeat(flatten(x / s))))).
+ * x_dev: [m][k] of x_dtype (F64/F32/F16/BF16), y_dev: [m][ldy] of y_dtype
+ * (F64/F32/F16/BF16, or I32 for the raw accumulators). bias_dev: optional
+ * [n] of bias_dtype (build extension; the reference has no bias).
+ * saturation_dev: optional device uint64 the call ADDS its saturation events
+ * to (pipeline.hpp:80-82). Asynchronous on `stream`. */
+int fqg_layer_forward(fqg_layer_t layer, const void* x_dev, int x_dtype, int64_t m, void* y_dev,
+                      int y_dtype, int64_t ldy, const void* bias_dev, int bias_dtype,
+                      unsigned long long* saturation_dev, void* stream);
+
+/* The drop-in host call: same contract as fq::run_layer(cfg, x, saturation)
+ * (pipeline.hpp:84) on host f64 buffers; copies in, runs, copies out,
+ * synchronizes. y_host: [m][n] f64, equal to the reference bit for bit. */
+int fqg_layer_run_host(fqg_layer_t layer, const double* x_host, int64_t m, double* y_host,
+                       int64_t* saturation);
+
+/* The activation half of run_layer (pipeline.cpp:164-167, i.e. divide_columns
+ * -> flatten_tensor(saturating) -> repeat_columns -> quantize_per_tensor):
+ * writes the quantized operand q_dev [m][K'] int8 (a_format I8) or
+ * [m][K'/2] packed int4 (a_format I4). */
+int fqg_layer_quantize_acts(fqg_layer_t layer, const void* x_dev, int x_dtype, int64_t m,
+                            void* q_dev, unsigned long long* saturation_dev, void* stream);
+
+/* The GEMM half (int_matmul, quantize.cpp:190-198) on an operand produced by
+ * fqg_layer_quantize_acts. */
+int fqg_layer_gemm(fqg_layer_t layer, const void* q_dev, int64_t m, void* y_dev, int y_dtype,
+                   int64_t ldy, const void* bias_dev, int bias_dtype, void* stream);
+
+/* Standalone integer GEMM (int_matmul_raw / int_matmul, quantize.cpp:166-198):
+ * a_dev [m][lda] and b_dev [n][ldb] K-major int8 (or packed int4), y as in
+ * fqg_layer_forward; scale_dev: device double[3] = {s_x, s_w, s_x*s_w}. */
+int fqg_gemm(const void* a_dev, int a_fmt, int64_t lda, const void* b_dev, int b_fmt, int64_t ldb,
+             int64_t m, int64_t n, int64_t kp, void* y_dev, int y_dtype, int64_t ldy,
+             const double* scale_dev, const void* bias_dev, int bias_dtype, void* stream);
+
+/* Host-side plan arithmetic (pure integer/FP64 work, no device):
+ * fq::build_flatten_plan (flatten.cpp:17-45). e/off: [k]. */
+int fqg_build_flatten_plan(const double* maxes, int64_t k, double t, int64_t block, int64_t* e,
+                           int64_t* off, int64_t* c_extend, int64_t* padded_width);
+/* fq::split_against_threshold (flatten.cpp:8-15). */
+void fqg_split_against_threshold(double abs_value, double t, int64_t* count, double* rem);
+
+/* Offline recipe builder for modes O1/O2 with the bit width pinned by the
+ * caller (KL bit selection, select_bit_width, is out of scope): the same
+ * stage order as fq::quantize_layer (pipeline.cpp:76-152). Channel maxima of
+ * the calibration set are given (collect_channel_maxes, calibration.cpp:9-28,
+ * see fqg_collect_channel_maxes); the weight W is host f64 [k][n]. Writes the
+ * recipe arrays: s[k], *t_x, e_x[k], *t_w, e_w[c1] (caller sizes e_w with
+ * fqg_recipe_plan_sizes), *act_scale. The weight tail then runs in
+ * fqg_layer_create with desc.weight = W. */
+int fqg_recipe_plan(const double* weight, int64_t k, int64_t n, const double* act_maxes, int bits,
+                    double alpha, double beta, int64_t block, int smooth, int clip, double* s,
+                    double* t_x, int64_t* e_x, int64_t* c1, double* t_w, int64_t* e_w,
+                    int64_t e_w_capacity, int64_t* kp, double* act_scale);
+void fqg_collect_channel_maxes(const double* calib, int64_t rows, int64_t k, double* maxes_inout);
+
+/* Deterministic synthetic layer generator with planted outlier channels, the
+ * reference's input substrate (fq::make_synthetic_layer, synthetic.cpp:54-92,
+ * mt19937_64 + Box-Muller). weight [k][n], calib [samples][rows][k],
+ * test_input [test_rows][k] (test_rows may differ from rows). */
+typedef struct fqg_synth_opts {
+    int64_t rows, samples, in_channels, out_channels;
+    double outlier_fraction, outlier_min, outlier_max, channel_spread;
+    double act_tail_prob_max, act_tail_scale, weight_row_spread;
+    uint64_t seed;
+} fqg_synth_opts;
+void fqg_synth_default(fqg_synth_opts* o);
+int fqg_synthetic_layer(const fqg_synth_opts* o, int64_t index, double* weight, double* calib,
+                        double* test_input, int64_t test_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FQG_H */

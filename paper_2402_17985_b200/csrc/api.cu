@@ -1,0 +1,61 @@
+// api.cu — the C ABI (include/fqg.h): error plumbing, device queries and the
+// standalone GEMM entry point. Layer handles live in layer.cu.
+#include <cstring>
+#include <string>
+
+#include "fqg_internal.h"
+
+namespace fqg {
+
+thread_local std::string g_last_error;
+
+int num_sms(int device) {
+    static int cache[64] = {0};
+    if (device < 0 || device >= 64) device = 0;
+    if (cache[device] == 0) {
+        int v = 0;
+        FQG_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+        cache[device] = v;
+    }
+    return cache[device];
+}
+
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return FQG_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return FQG_ERR_INVALID;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FQG_ERR_RUNTIME;
+    }
+}
+
+}  // namespace fqg
+
+using namespace fqg;
+
+extern "C" {
+
+const char* fqg_last_error(void) { return g_last_error.c_str(); }
+
+int fqg_version(void) { return 1; }
+
+int fqg_gemm(const void* a_dev, int a_fmt, int64_t lda, const void* b_dev, int b_fmt, int64_t ldb,
+             int64_t m, int64_t n, int64_t kp, void* y_dev, int y_dtype, int64_t ldy,
+             const double* scale_dev, const void* bias_dev, int bias_dtype, void* stream) {
+    return guard([&] {
+        GemmArgs g{a_dev, a_fmt, lda, b_dev, b_fmt, ldb, m, n, kp, y_dev, y_dtype, ldy,
+                   scale_dev, bias_dev, bias_dev ? bias_dtype : FQG_NONE};
+        require(y_dtype == FQG_I32 || scale_dev != nullptr, "fqg_gemm: scale_dev is required");
+        gemm_i8(g, static_cast<cudaStream_t>(stream));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,69 @@
+// fqg_internal.h — declarations shared by the host launcher code and the
+// kernels of libfqg (not part of the public C ABI in include/fqg.h).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+
+#include "../../include/fqg.h"
+
+namespace fqg {
+
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define FQG_CUDA(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = (expr);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            throw ::fqg::Error(FQG_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+inline void require(bool ok, const std::string& what) {
+    if (!ok) throw Error(FQG_ERR_INVALID, what);
+}
+
+inline int dtype_size(int dt) {
+    switch (dt) {
+        case FQG_F64: return 8;
+        case FQG_F32: return 4;
+        case FQG_F16: return 2;
+        case FQG_BF16: return 2;
+        case FQG_I32: return 4;
+        case FQG_I8: return 1;
+        default: return 0;
+    }
+}
+
+int num_sms(int device);
+
+// ---- K4: tcgen05 kind::i8 GEMM -------------------------------------------
+// Y[M, N] = epilogue( A[M, K'] . B[N, K']^T ), A/B K-major int8 or packed int4.
+struct GemmArgs {
+    const void* a;        // [M][lda] bytes, K-major
+    int a_fmt;            // FQG_I8 | FQG_I4 (two nibbles per byte, low = even k)
+    int64_t lda;          // row stride in bytes
+    const void* b;        // [N][ldb] bytes, K-major
+    int b_fmt;
+    int64_t ldb;
+    int64_t m, n, kp;     // kp = logical K' (elements)
+    void* y;
+    int y_dtype;          // FQG_F64/F32/F16/BF16 or FQG_I32 (raw accumulators)
+    int64_t ldy;          // elements
+    const double* scale;  // device: scale[0] = s_x, scale[1] = s_w, scale[2] = s_x*s_w
+    const void* bias;     // device [N] or nullptr
+    int bias_dtype;
+};
+void gemm_i8(const GemmArgs& g, cudaStream_t stream);
+
+// TMA descriptor construction through the driver entry point (no -lcuda).
+void make_tmap_2d_u8(CUtensorMap* map, const void* base, uint64_t inner_bytes, uint64_t rows,
+                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_rows,
+                     CUtensorMapSwizzle swz);
+
+}  // namespace fqg

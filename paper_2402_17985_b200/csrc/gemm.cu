@@ -1,0 +1,341 @@
+// gemm.cu — K4: the flattened low-bit GEMM on 5th-gen tensor cores.
+//
+//   Y[M,N] = epi( sum_k A[M,k] * B[N,k] ),  A,B int8 K-major, INT32 accumulate
+//
+// replaces fq::int_matmul_raw + fq::int_matmul (quantize.cpp:166-198). The
+// accumulators are exact int32 (|acc| <= K' * qmax^2 < 2^31 for K' <= 133144,
+// checked by the host), so the result is bit-identical to the reference's
+// int64 sums; the epilogue then forms y = double(acc) * (s_x * s_w) exactly as
+// quantize.cpp:193-196 does and rounds once to the output type.
+//
+// Structure (one CTA per SM, persistent over output tiles, 256 threads):
+//   warp 0 lane 0 : TMA producer — A tile 128x128B and B tile BNx128B per stage,
+//                   128-byte swizzle, OOB rows/cols zero-filled by the TMA unit
+//   warp 1        : TMEM allocator (2*BN columns: double-buffered accumulator);
+//                   lane 0 issues tcgen05.mma.cta_group::1.kind::i8 128xBNx32
+//   warps 4..7    : epilogue — tcgen05.ld 32x32b, dequant + bias, convert, store
+// Pipelines: smem ring full/empty mbarriers (TMA <-> MMA, tcgen05.commit frees a
+// slot), TMEM full/empty mbarriers (MMA <-> epilogue), so the epilogue of tile
+// i overlaps the main loop of tile i+1.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "fqg_internal.h"
+#include "ptx.cuh"
+
+namespace fqg {
+namespace {
+
+constexpr int BM = 128;       // UMMA M (cta_group::1)
+constexpr int BK = 128;       // K bytes per stage = one 128B swizzle row
+constexpr int UK = 32;        // K per tcgen05.mma kind::i8
+constexpr int kThreads = 256;
+
+template <int BN, int STAGES>
+struct Layout {
+    static constexpr int a_bytes = BM * BK;
+    static constexpr int b_bytes = BN * BK;
+    static constexpr int stage_bytes = a_bytes + b_bytes;
+    static constexpr int bar_off = STAGES * stage_bytes;
+    static constexpr int bar_bytes = (2 * STAGES + 4) * 8 + 16;
+    static constexpr int total = bar_off + bar_bytes + 1024;  // + alignment slack
+};
+
+__device__ __forceinline__ double load_bias(const void* bias, int dt, int col) {
+    switch (dt) {
+        case FQG_F32: return static_cast<double>(static_cast<const float*>(bias)[col]);
+        case FQG_F64: return static_cast<const double*>(bias)[col];
+        case FQG_F16: return static_cast<double>(__half2float(static_cast<const __half*>(bias)[col]));
+        case FQG_BF16:
+            return static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(bias)[col]));
+        default: return 0.0;
+    }
+}
+
+template <int OUT>
+__device__ __forceinline__ void store_one(void* y, int64_t idx, int32_t acc, double s, double b) {
+    if constexpr (OUT == FQG_I32) {
+        static_cast<int32_t*>(y)[idx] = acc;
+    } else {
+        // quantize.cpp:196: out = double(acc) * (s_x * s_w); + bias extension.
+        const double v = static_cast<double>(acc) * s + b;
+        if constexpr (OUT == FQG_F64) static_cast<double*>(y)[idx] = v;
+        if constexpr (OUT == FQG_F32) static_cast<float*>(y)[idx] = static_cast<float>(v);
+        if constexpr (OUT == FQG_F16) static_cast<__half*>(y)[idx] = __double2half(v);
+        if constexpr (OUT == FQG_BF16) static_cast<__nv_bfloat16*>(y)[idx] = __double2bfloat16(v);
+    }
+}
+
+// 32 consecutive columns of one row, from 32 accumulator registers.
+template <int OUT>
+__device__ __forceinline__ void store_row_chunk(void* y, int64_t base, const uint32_t (&r)[32],
+                                                double s, const void* bias, int bias_dt, int col0,
+                                                int ncols, bool vec) {
+    if (vec && ncols == 32) {
+        if constexpr (OUT == FQG_I32) {
+            int4* p = reinterpret_cast<int4*>(static_cast<int32_t*>(y) + base);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                p[q] = make_int4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+            return;
+        } else if constexpr (OUT == FQG_F16 || OUT == FQG_BF16) {
+            uint32_t packed[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                double v0 = static_cast<double>(static_cast<int32_t>(r[2 * q])) * s;
+                double v1 = static_cast<double>(static_cast<int32_t>(r[2 * q + 1])) * s;
+                if (bias) {
+                    v0 += load_bias(bias, bias_dt, col0 + 2 * q);
+                    v1 += load_bias(bias, bias_dt, col0 + 2 * q + 1);
+                }
+                if constexpr (OUT == FQG_F16) {
+                    __half2 h = __halves2half2(__double2half(v0), __double2half(v1));
+                    packed[q] = *reinterpret_cast<uint32_t*>(&h);
+                } else {
+                    __nv_bfloat162 h;
+                    h.x = __double2bfloat16(v0);
+                    h.y = __double2bfloat16(v1);
+                    packed[q] = *reinterpret_cast<uint32_t*>(&h);
+                }
+            }
+            uint4* p = reinterpret_cast<uint4*>(static_cast<uint16_t*>(y) + base);
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                p[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
+                                  packed[4 * q + 3]);
+            return;
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 32; ++c) {
+        if (c < ncols) {
+            const double b = bias ? load_bias(bias, bias_dt, col0 + c) : 0.0;
+            store_one<OUT>(y, base + c, static_cast<int32_t>(r[c]), s, b);
+        }
+    }
+}
+
+template <int BN, int STAGES, int OUT>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
+              const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
+              int vec_ok) {
+    using L = Layout<BN, STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int num_m = (m + BM - 1) / BM;
+    const int num_n = (n + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+
+    if (threadIdx.x == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(tmem_holder, 2 * BN);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        const uint64_t keep = ptx::policy_evict_last();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int m_blk = tile % num_m, n_blk = tile / num_m;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem + stage * L::stage_bytes;
+                uint8_t* sb = sa + L::a_bytes;
+                ptx::mbar_arrive_expect_tx(&full[stage], L::stage_bytes);
+                ptx::tma_load_2d_hint(sa, &tmA, &full[stage], kb * BK, m_blk * BM, keep);
+                ptx::tma_load_2d_hint(sb, &tmB, &full[stage], kb * BK, n_blk * BN, keep);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+        int stage = 0;
+        uint32_t phase = 0;
+        int it = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                ptx::mbar_wait(&full[stage], phase);
+                ptx::tc_fence_after();
+                const uint32_t a_addr = ptx::smem_u32(smem + stage * L::stage_bytes);
+                const uint32_t b_addr = a_addr + L::a_bytes;
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k) {
+                    ptx::mma_i8(d_tmem, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
+                                ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
+                                (kb | k) != 0 ? 1u : 0u);
+                }
+                ptx::mma_commit(&empty[stage]);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            ptx::mma_commit(&tfull[acc]);
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue ----------------
+        const int ew = warp - 4;  // TMEM lane quarter this warp may access
+        const double s = OUT == FQG_I32 ? 1.0 : scale[2];
+        int it = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            const int m_blk = tile % num_m, n_blk = tile / num_m;
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            const int row = m_blk * BM + ew * 32 + lane;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+                ptx::tmem_wait_ld();
+                const int col0 = n_blk * BN + c * 32;
+                if (row < m && col0 < n) {
+                    const int ncols = min(32, n - col0);
+                    store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
+                                         bias_dt, col0, ncols, vec_ok != 0);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 2 * BN);
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
+    return fn;
+}
+
+template <int BN, int STAGES, int OUT>
+void launch(const GemmArgs& g, cudaStream_t stream) {
+    using L = Layout<BN, STAGES>;
+    CUtensorMap ta, tb;
+    make_tmap_2d_u8(&ta, g.a, static_cast<uint64_t>(g.kp), static_cast<uint64_t>(g.m),
+                    static_cast<uint64_t>(g.lda), BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
+    make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(g.kp), static_cast<uint64_t>(g.n),
+                    static_cast<uint64_t>(g.ldb), BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    auto kern = k_gemm_i8<BN, STAGES, OUT>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        attr_set = true;
+    }
+    int dev = 0;
+    FQG_CUDA(cudaGetDevice(&dev));
+    const int num_tiles = static_cast<int>(((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN));
+    const int grid = std::max(1, std::min(num_tiles, num_sms(dev)));
+    const int esz = dtype_size(g.y_dtype);
+    const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
+    const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
+    kern<<<grid, kThreads, L::total, stream>>>(ta, tb, g.y, g.ldy, static_cast<int>(g.m),
+                                              static_cast<int>(g.n), num_kb, g.scale, g.bias,
+                                              g.bias_dtype, vec ? 1 : 0);
+    FQG_CUDA(cudaGetLastError());
+}
+
+template <int BN>
+void dispatch_out(const GemmArgs& g, cudaStream_t s) {
+    constexpr int ST = 4;
+    switch (g.y_dtype) {
+        case FQG_I32: return launch<BN, ST, FQG_I32>(g, s);
+        case FQG_F64: return launch<BN, ST, FQG_F64>(g, s);
+        case FQG_F32: return launch<BN, ST, FQG_F32>(g, s);
+        case FQG_F16: return launch<BN, ST, FQG_F16>(g, s);
+        case FQG_BF16: return launch<BN, ST, FQG_BF16>(g, s);
+        default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
+    }
+}
+
+}  // namespace
+
+void make_tmap_2d_u8(CUtensorMap* map, const void* base, uint64_t inner_bytes, uint64_t rows,
+                     uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_rows,
+                     CUtensorMapSwizzle swz) {
+    require(reinterpret_cast<uintptr_t>(base) % 16 == 0, "tma: base must be 16-byte aligned");
+    require(row_stride_bytes % 16 == 0, "tma: row stride must be a multiple of 16 bytes");
+    const cuuint64_t dims[2] = {inner_bytes, rows};
+    const cuuint64_t strides[1] = {row_stride_bytes};
+    const cuuint32_t box[2] = {box_inner, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r =
+        encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides,
+                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(r) + ")");
+}
+
+void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
+    require(g.m >= 1 && g.n >= 1 && g.kp >= 1, "gemm: empty shape");
+    require(g.m < (1ll << 31) && g.n < (1ll << 31), "gemm: shape too large");
+    require(g.a_fmt == FQG_I8 && g.b_fmt == FQG_I8, "gemm: this build takes int8 operands");
+    require(g.kp % 16 == 0, "gemm: K' must be a multiple of 16");
+    // INT32 exactness: |acc| <= K' * 127 * 127 must stay below 2^31.
+    require(g.kp * 127ll * 127ll < (1ll << 31), "gemm: K' too large for exact INT32 accumulation");
+    if (g.n <= 128)
+        dispatch_out<128>(g, stream);
+    else
+        dispatch_out<256>(g, stream);
+}
+
+}  // namespace fqg

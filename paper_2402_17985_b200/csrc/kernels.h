@@ -1,0 +1,37 @@
+// kernels.h — launch interfaces of the HBM-bound kernels in flatten.cu.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace fqg {
+
+struct FlattenArgs {
+    const void* x;                // [m][ldx] activations
+    int x_dtype;                  // FQG_F64/F32/F16/BF16
+    int64_t ldx;                  // elements
+    int64_t m, k, kp;
+    const double* s;              // [k] smoothing scales
+    const int32_t* cap;           // [k] plan_x capacity E_x + 1
+    const int32_t* amap;          // [kp] (j << 12 | p) or -1
+    double t;                     // plan_x threshold T_x
+    double* scale;                // device; [0] = s_x (read; written in dynamic mode)
+    unsigned long long* amax;     // dynamic mode: zeroed absmax cell, else nullptr
+    double qmax;
+    bool pack4;                   // packed int4 output
+    uint8_t* q;                   // [m][ldq] bytes
+    int64_t ldq;
+    unsigned long long* sat;      // optional saturation accumulator
+    int num_sms;
+};
+void flatten_quant(const FlattenArgs& a, cudaStream_t st);
+
+void weight_absmax(const double* w, int64_t k, int64_t ncols, const double* s,
+                   const int32_t* capw_src, double t_w, unsigned long long* amax,
+                   unsigned int* overflow, int num_sms, cudaStream_t st);
+
+void weight_quant(const double* w, int64_t ldw, int64_t n_begin, int64_t n, const double* s,
+                  const int32_t* wmap, const int32_t* wcap, int64_t kp, double t_w, double s_w,
+                  double qmax, bool pack4, uint8_t* wq, int64_t ldq, cudaStream_t st);
+
+}  // namespace fqg
