@@ -137,7 +137,7 @@ int fqg_layer_gemm(fqg_layer_t layer, const void* q_dev, int64_t m, void* y_dev,
 
 /* Standalone integer GEMM (int_matmul_raw / int_matmul, quantize.cpp:166-198):
  * a_dev [m][lda] and b_dev [n][ldb] K-major int8 (or packed int4), y as in
- * fqg_layer_forward; scale_dev: device double[3] = {s_x, s_w, s_x*s_w}. */
+ * fqg_layer_forward; scale_dev: device double[2] = {s_x, s_w}; the epilogue forms s_x*s_w once in FP64 (quantize.cpp:193). */
 int fqg_gemm(const void* a_dev, int a_fmt, int64_t lda, const void* b_dev, int b_fmt, int64_t ldb,
              int64_t m, int64_t n, int64_t kp, void* y_dev, int y_dtype, int64_t ldy,
              const double* scale_dev, const void* bias_dev, int bias_dtype, void* stream);

@@ -20,23 +20,6 @@ int num_sms(int device) {
     return cache[device];
 }
 
-template <class F>
-int guard(F&& f) {
-    try {
-        f();
-        return FQG_OK;
-    } catch (const Error& e) {
-        g_last_error = e.what();
-        return e.code;
-    } catch (const std::invalid_argument& e) {
-        g_last_error = e.what();
-        return FQG_ERR_INVALID;
-    } catch (const std::exception& e) {
-        g_last_error = e.what();
-        return FQG_ERR_RUNTIME;
-    }
-}
-
 }  // namespace fqg
 
 using namespace fqg;

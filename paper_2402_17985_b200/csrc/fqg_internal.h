@@ -42,6 +42,26 @@ inline int dtype_size(int dt) {
 
 int num_sms(int device);
 
+extern thread_local std::string g_last_error;
+
+// Runs f, converting exceptions into fqg_status codes + fqg_last_error().
+template <class F>
+int guard(F&& f) {
+    try {
+        f();
+        return FQG_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        g_last_error = e.what();
+        return FQG_ERR_INVALID;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return FQG_ERR_RUNTIME;
+    }
+}
+
 // ---- K4: tcgen05 kind::i8 GEMM -------------------------------------------
 // Y[M, N] = epilogue( A[M, K'] . B[N, K']^T ), A/B K-major int8 or packed int4.
 struct GemmArgs {
@@ -55,7 +75,7 @@ struct GemmArgs {
     void* y;
     int y_dtype;          // FQG_F64/F32/F16/BF16 or FQG_I32 (raw accumulators)
     int64_t ldy;          // elements
-    const double* scale;  // device: scale[0] = s_x, scale[1] = s_w, scale[2] = s_x*s_w
+    const double* scale;  // device: scale[0] = s_x, scale[1] = s_w
     const void* bias;     // device [N] or nullptr
     int bias_dtype;
 };

@@ -33,17 +33,67 @@ namespace {
 constexpr int BM = 128;       // UMMA M (cta_group::1)
 constexpr int BK = 128;       // K bytes per stage = one 128B swizzle row
 constexpr int UK = 32;        // K per tcgen05.mma kind::i8
-constexpr int kThreads = 256;
 
-template <int BN, int STAGES>
+// Shared-memory plan. The "raw" ring is what the TMA writes: int8 operands in
+// the 128B-swizzled UMMA layout, packed int4 operands as plain 64-byte rows.
+// With a packed operand, unpack warps expand it into the "unpacked" ring
+// (int8, 128B-swizzled) before the MMA reads it.
+template <int BN, int STAGES, bool APK, bool BPK>
 struct Layout {
-    static constexpr int a_bytes = BM * BK;
-    static constexpr int b_bytes = BN * BK;
-    static constexpr int stage_bytes = a_bytes + b_bytes;
-    static constexpr int bar_off = STAGES * stage_bytes;
-    static constexpr int bar_bytes = (2 * STAGES + 4) * 8 + 16;
-    static constexpr int total = bar_off + bar_bytes + 1024;  // + alignment slack
+    static constexpr bool packed = APK || BPK;
+    static constexpr int a_raw = APK ? BM * BK / 2 : BM * BK;
+    static constexpr int b_raw = BPK ? BN * BK / 2 : BN * BK;
+    static constexpr int raw_stage = a_raw + b_raw;  // multiple of 1024
+    static constexpr int USTAGES = packed ? 2 : 0;
+    static constexpr int a_unp = APK ? BM * BK : 0;
+    static constexpr int b_unp = BPK ? BN * BK : 0;
+    static constexpr int unp_stage = a_unp + b_unp;
+    static constexpr int unp_off = STAGES * raw_stage;
+    static constexpr int bar_off = unp_off + USTAGES * unp_stage;
+    static constexpr int n_bars = 2 * STAGES + 2 * USTAGES + 4;
+    static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;  // + alignment slack
+    static constexpr int unpack_warps = packed ? 4 : 0;
+    static constexpr int threads = 256 + 32 * unpack_warps;
+    // Arrivals that free a raw stage: the MMA commit if it reads an int8
+    // operand straight from the raw stage, plus one per unpack warp.
+    static constexpr int raw_release = (APK && BPK ? 0 : 1) + unpack_warps;
 };
+
+// 16 packed bytes (32 int4, low nibble = even k) -> 32 int8 in k order.
+// Per nibble v: ((v ^ 8) + 0x78) ^ 0x80 is v sign-extended, with no carry
+// between byte lanes ((v ^ 8) + 0x78 <= 0x87).
+__device__ __forceinline__ uint32_t sext4x4(uint32_t nib) {
+    return ((nib ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
+}
+__device__ __forceinline__ void unpack16(uint4 p, uint4& o0, uint4& o1) {
+    const uint32_t w[4] = {p.x, p.y, p.z, p.w};
+    uint32_t o[8];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t lo = sext4x4(w[i] & 0x0F0F0F0Fu);
+        const uint32_t hi = sext4x4((w[i] >> 4) & 0x0F0F0F0Fu);
+        o[2 * i] = __byte_perm(lo, hi, 0x5140);
+        o[2 * i + 1] = __byte_perm(lo, hi, 0x7362);
+    }
+    o0 = make_uint4(o[0], o[1], o[2], o[3]);
+    o1 = make_uint4(o[4], o[5], o[6], o[7]);
+}
+
+// Expand `rows` x 64 packed bytes (plain rows) into rows x 128 int8 in the
+// 128B-swizzle K-major layout: 16-byte chunk c of row r at r*128 + ((c ^ r%8) * 16).
+__device__ __forceinline__ void unpack_tile(const uint8_t* src, uint8_t* dst, int rows, int tid,
+                                            int nthreads) {
+    for (int u = tid; u < rows * 4; u += nthreads) {
+        const int r = u >> 2, pc = u & 3;
+        const uint4 p = *reinterpret_cast<const uint4*>(src + r * 64 + pc * 16);
+        uint4 o0, o1;
+        unpack16(p, o0, o1);
+        uint8_t* row = dst + r * 128;
+        const int c0 = 2 * pc, c1 = 2 * pc + 1, sw = r & 7;
+        *reinterpret_cast<uint4*>(row + ((c0 ^ sw) << 4)) = o0;
+        *reinterpret_cast<uint4*>(row + ((c1 ^ sw) << 4)) = o1;
+    }
+}
 
 __device__ __forceinline__ double load_bias(const void* bias, int dt, int col) {
     switch (dt) {
@@ -119,19 +169,22 @@ __device__ __forceinline__ void store_row_chunk(void* y, int64_t base, const uin
     }
 }
 
-template <int BN, int STAGES, int OUT>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int STAGES, int OUT, bool APK, bool BPK>
+__global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
     k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
               const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
               int vec_ok) {
-    using L = Layout<BN, STAGES>;
+    using L = Layout<BN, STAGES, APK, BPK>;
+    constexpr int U = L::USTAGES;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);
     uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint64_t* ufull = empty + STAGES;   // [U] unpacked stage ready
+    uint64_t* uempty = ufull + U;       // [U] unpacked stage consumed by the MMA
+    uint64_t* tfull = uempty + U;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -145,7 +198,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tma_prefetch_desc(&tmB);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], 1);
+            ptx::mbar_init(&empty[s], L::raw_release);
+        }
+        for (int u = 0; u < U; ++u) {
+            ptx::mbar_init(&ufull[u], L::unpack_warps);
+            ptx::mbar_init(&uempty[u], 1);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
@@ -171,11 +228,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             for (int kb = 0; kb < num_kb; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
-                uint8_t* sa = smem + stage * L::stage_bytes;
-                uint8_t* sb = sa + L::a_bytes;
-                ptx::mbar_arrive_expect_tx(&full[stage], L::stage_bytes);
-                ptx::tma_load_2d_hint(sa, &tmA, &full[stage], kb * BK, m_blk * BM, keep);
-                ptx::tma_load_2d_hint(sb, &tmB, &full[stage], kb * BK, n_blk * BN, keep);
+                uint8_t* sa = smem + stage * L::raw_stage;
+                uint8_t* sb = sa + L::a_raw;
+                ptx::mbar_arrive_expect_tx(&full[stage], L::raw_stage);
+                ptx::tma_load_2d_hint(sa, &tmA, &full[stage], kb * (APK ? BK / 2 : BK), m_blk * BM,
+                                      keep);
+                ptx::tma_load_2d_hint(sb, &tmB, &full[stage], kb * (BPK ? BK / 2 : BK), n_blk * BN,
+                                      keep);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -185,8 +244,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
         constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
-        int stage = 0;
-        uint32_t phase = 0;
+        int stage = 0, us = 0;
+        uint32_t phase = 0, uphase = 0;
         int it = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
             const int acc = it & 1;
@@ -196,16 +255,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t d_tmem = tmem_base + acc * BN;
             for (int kb = 0; kb < num_kb; ++kb) {
                 ptx::mbar_wait(&full[stage], phase);
+                if constexpr (L::packed) ptx::mbar_wait(&ufull[us], uphase);
                 ptx::tc_fence_after();
-                const uint32_t a_addr = ptx::smem_u32(smem + stage * L::stage_bytes);
-                const uint32_t b_addr = a_addr + L::a_bytes;
+                const uint32_t raw = ptx::smem_u32(smem + stage * L::raw_stage);
+                const uint32_t unp = ptx::smem_u32(smem + L::unp_off + us * L::unp_stage);
+                const uint32_t a_addr = APK ? unp : raw;
+                const uint32_t b_addr = BPK ? unp + L::a_unp : raw + L::a_raw;
 #pragma unroll
                 for (int k = 0; k < BK / UK; ++k) {
                     ptx::mma_i8(d_tmem, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
                                 ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
                                 (kb | k) != 0 ? 1u : 0u);
                 }
-                ptx::mma_commit(&empty[stage]);
+                if constexpr (!(APK && BPK)) ptx::mma_commit(&empty[stage]);
+                if constexpr (L::packed) {
+                    ptx::mma_commit(&uempty[us]);
+                    if (++us == U) {
+                        us = 0;
+                        uphase ^= 1;
+                    }
+                }
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -213,10 +282,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::mma_commit(&tfull[acc]);
         }
-    } else if (warp >= 4) {
+    } else if (warp >= 4 && warp < 8) {
         // ---------------- epilogue ----------------
         const int ew = warp - 4;  // TMEM lane quarter this warp may access
-        const double s = OUT == FQG_I32 ? 1.0 : scale[2];
+        // quantize.cpp:193: the product s_x * s_w formed once in FP64.
+        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
         int it = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
@@ -242,6 +312,36 @@ __global__ void __launch_bounds__(kThreads, 1)
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
         }
+    } else if (L::packed && warp >= 8) {
+        // ---------------- int4 -> int8 unpack warps ----------------
+        const int utid = threadIdx.x - 256, nut = 32 * L::unpack_warps;
+        int stage = 0, us = 0;
+        uint32_t phase = 0, uphase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (int kb = 0; kb < num_kb; ++kb) {
+                ptx::mbar_wait(&full[stage], phase);
+                ptx::mbar_wait(&uempty[us], uphase ^ 1);
+                const uint8_t* raw = smem + stage * L::raw_stage;
+                uint8_t* unp = smem + L::unp_off + us * L::unp_stage;
+                if constexpr (APK) unpack_tile(raw, unp, BM, utid, nut);
+                if constexpr (BPK) unpack_tile(raw + L::a_raw, unp + L::a_unp, BN, utid, nut);
+                // generic-proxy smem writes -> visible to the tensor core (async proxy)
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(&ufull[us]);
+                    ptx::mbar_arrive(&empty[stage]);
+                }
+                if (++us == U) {
+                    us = 0;
+                    uphase ^= 1;
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
     }
     __syncthreads();
     if (warp == 1) {
@@ -266,15 +366,19 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int BN, int STAGES, int OUT>
+template <int BN, int STAGES, int OUT, bool APK, bool BPK>
 void launch(const GemmArgs& g, cudaStream_t stream) {
-    using L = Layout<BN, STAGES>;
+    using L = Layout<BN, STAGES, APK, BPK>;
+    static_assert(L::total <= 227 * 1024, "shared memory budget");
     CUtensorMap ta, tb;
-    make_tmap_2d_u8(&ta, g.a, static_cast<uint64_t>(g.kp), static_cast<uint64_t>(g.m),
-                    static_cast<uint64_t>(g.lda), BK, BM, CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(g.kp), static_cast<uint64_t>(g.n),
-                    static_cast<uint64_t>(g.ldb), BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
-    auto kern = k_gemm_i8<BN, STAGES, OUT>;
+    // Logical K extent in bytes: the TMA zero-fills K' .. ceil(K', 128).
+    make_tmap_2d_u8(&ta, g.a, static_cast<uint64_t>(APK ? g.kp / 2 : g.kp),
+                    static_cast<uint64_t>(g.m), static_cast<uint64_t>(g.lda), APK ? BK / 2 : BK,
+                    BM, APK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
+    make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(BPK ? g.kp / 2 : g.kp),
+                    static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.ldb), BPK ? BK / 2 : BK,
+                    BN, BPK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
+    auto kern = k_gemm_i8<BN, STAGES, OUT, APK, BPK>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
@@ -287,23 +391,32 @@ void launch(const GemmArgs& g, cudaStream_t stream) {
     const int esz = dtype_size(g.y_dtype);
     const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
     const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
-    kern<<<grid, kThreads, L::total, stream>>>(ta, tb, g.y, g.ldy, static_cast<int>(g.m),
-                                              static_cast<int>(g.n), num_kb, g.scale, g.bias,
-                                              g.bias_dtype, vec ? 1 : 0);
+    kern<<<grid, L::threads, L::total, stream>>>(ta, tb, g.y, g.ldy, static_cast<int>(g.m),
+                                                 static_cast<int>(g.n), num_kb, g.scale, g.bias,
+                                                 g.bias_dtype, vec ? 1 : 0);
     FQG_CUDA(cudaGetLastError());
 }
 
-template <int BN>
+template <int BN, bool APK, bool BPK>
 void dispatch_out(const GemmArgs& g, cudaStream_t s) {
-    constexpr int ST = 4;
+    constexpr int ST = (APK || BPK) ? 4 : 4;
     switch (g.y_dtype) {
-        case FQG_I32: return launch<BN, ST, FQG_I32>(g, s);
-        case FQG_F64: return launch<BN, ST, FQG_F64>(g, s);
-        case FQG_F32: return launch<BN, ST, FQG_F32>(g, s);
-        case FQG_F16: return launch<BN, ST, FQG_F16>(g, s);
-        case FQG_BF16: return launch<BN, ST, FQG_BF16>(g, s);
+        case FQG_I32: return launch<BN, ST, FQG_I32, APK, BPK>(g, s);
+        case FQG_F64: return launch<BN, ST, FQG_F64, APK, BPK>(g, s);
+        case FQG_F32: return launch<BN, ST, FQG_F32, APK, BPK>(g, s);
+        case FQG_F16: return launch<BN, ST, FQG_F16, APK, BPK>(g, s);
+        case FQG_BF16: return launch<BN, ST, FQG_BF16, APK, BPK>(g, s);
         default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
     }
+}
+
+template <int BN>
+void dispatch_fmt(const GemmArgs& g, cudaStream_t s) {
+    const bool apk = g.a_fmt == FQG_I4, bpk = g.b_fmt == FQG_I4;
+    if (!apk && !bpk) return dispatch_out<BN, false, false>(g, s);
+    if (!apk && bpk) return dispatch_out<BN, false, true>(g, s);
+    if (apk && !bpk) return dispatch_out<BN, true, false>(g, s);
+    return dispatch_out<BN, true, true>(g, s);
 }
 
 }  // namespace
@@ -328,14 +441,15 @@ void make_tmap_2d_u8(CUtensorMap* map, const void* base, uint64_t inner_bytes, u
 void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
     require(g.m >= 1 && g.n >= 1 && g.kp >= 1, "gemm: empty shape");
     require(g.m < (1ll << 31) && g.n < (1ll << 31), "gemm: shape too large");
-    require(g.a_fmt == FQG_I8 && g.b_fmt == FQG_I8, "gemm: this build takes int8 operands");
-    require(g.kp % 16 == 0, "gemm: K' must be a multiple of 16");
+    require(g.a_fmt == FQG_I8 || g.a_fmt == FQG_I4, "gemm: operand A must be I8 or I4");
+    require(g.b_fmt == FQG_I8 || g.b_fmt == FQG_I4, "gemm: operand B must be I8 or I4");
+    require(g.kp % 32 == 0, "gemm: K' must be a multiple of 32");
     // INT32 exactness: |acc| <= K' * 127 * 127 must stay below 2^31.
     require(g.kp * 127ll * 127ll < (1ll << 31), "gemm: K' too large for exact INT32 accumulation");
     if (g.n <= 128)
-        dispatch_out<128>(g, stream);
+        dispatch_fmt<128>(g, stream);
     else
-        dispatch_out<256>(g, stream);
+        dispatch_fmt<256>(g, stream);
 }
 
 }  // namespace fqg

@@ -1,0 +1,374 @@
+// layer.cu — the layer handle behind the C ABI: a frozen, device-resident
+// recipe (fq::LayerQuantConfig, pipeline.hpp:37-49) and the forward pass that
+// replaces fq::run_layer (pipeline.cpp:159-169).
+//
+// HBM layout per layer:
+//   d_s    f64 [K]        smoothing scales (divide, smoothing.cpp:75)
+//   d_cap  i32 [K]        plan_x capacity E_x + 1
+//   d_amap i32 [K']       composite activation gather map (j << 12 | piece)
+//   d_wq   u8  [N][ldb]   weights, K-major: int8 (ldb = K') or packed int4 (K'/2)
+//   d_scale f64 [2]       {s_x, s_w}
+// Per forward (stream-ordered allocations): q [M][ldq] int8 / packed int4.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "fqg_internal.h"
+#include "host.h"
+#include "kernels.h"
+
+namespace fqg {
+
+struct DevBuf {
+    void* p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    void alloc(size_t bytes) { FQG_CUDA(cudaMalloc(&p, std::max<size_t>(bytes, 16))); }
+};
+
+}  // namespace fqg
+
+struct fqg_layer_s {
+    int device = 0;
+    int bits = 8, a_fmt = FQG_I8, b_fmt = FQG_I8, scale_mode = FQG_SCALE_STATIC;
+    int64_t k = 0, n = 0, c1 = 0, kp = 0, n_total = 0, n_begin = 0;
+    int64_t ldb = 0;
+    double t_x = 0, t_w = 0, act_scale = 0, w_scale = 0, qmax = 127;
+    fqg::DevBuf d_s, d_cap, d_amap, d_wq, d_scale;
+};
+
+namespace fqg {
+namespace {
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        FQG_CUDA(cudaGetDevice(&prev));
+        if (prev != dev) FQG_CUDA(cudaSetDevice(dev));
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (cudaGetDevice(&cur) == cudaSuccess && cur != prev && prev >= 0) cudaSetDevice(prev);
+    }
+};
+
+template <class T>
+void upload(DevBuf& b, const std::vector<T>& v) {
+    b.alloc(v.size() * sizeof(T));
+    FQG_CUDA(cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+}
+
+// int32 [K'][n_total] row-major (reference weight_q) -> K-major int8/int4 [n][ldb].
+std::vector<uint8_t> pack_weight_q(const int32_t* wq, int64_t kp, int64_t n_total, int64_t n_begin,
+                                   int64_t n, int qmax, bool pack4, int64_t ldb) {
+    std::vector<uint8_t> out(static_cast<size_t>(n * ldb), 0);
+    for (int64_t kq = 0; kq < kp; ++kq) {
+        const int32_t* row = wq + kq * n_total + n_begin;
+        for (int64_t c = 0; c < n; ++c) {
+            const int32_t v = row[c];
+            require(v >= -qmax && v <= qmax, "weight_q value outside [-qmax, qmax]");
+            if (pack4) {
+                uint8_t& b = out[c * ldb + kq / 2];
+                b |= static_cast<uint8_t>((v & 0xF) << ((kq & 1) * 4));
+            } else {
+                out[c * ldb + kq] = static_cast<uint8_t>(static_cast<int8_t>(v));
+            }
+        }
+    }
+    return out;
+}
+
+fqg_layer_s* create(const fqg_layer_desc& d) {
+    require(d.bits == 4 || d.bits == 8, "bits must be 4 or 8");
+    require(d.k >= 1 && d.n >= 1, "layer: empty shape");
+    require(d.smooth_scales && d.ext_x && d.ext_w, "layer: recipe arrays are required");
+    require(d.weight_q || d.weight, "layer: weight_q or weight is required");
+    require(d.t_x > 0.0 && std::isfinite(d.t_x), "layer: t_x must be > 0");
+    require(d.a_format == FQG_I8 || d.a_format == FQG_I4, "layer: a_format must be I8 or I4");
+    require(d.b_format == FQG_I8 || d.b_format == FQG_I4, "layer: b_format must be I8 or I4");
+    require(d.bits == 4 || (d.a_format == FQG_I8 && d.b_format == FQG_I8),
+            "layer: packed int4 operands need bits == 4");
+    require(d.scale_mode == FQG_SCALE_STATIC || d.scale_mode == FQG_SCALE_DYNAMIC,
+            "layer: bad scale_mode");
+    const int64_t n_total = d.n_total > 0 ? d.n_total : d.n;
+    require(d.n_begin >= 0 && d.n_begin + d.n <= n_total, "layer: shard outside [0, n_total)");
+    if (d.scale_mode == FQG_SCALE_STATIC)
+        require(d.act_scale > 0.0 && std::isfinite(d.act_scale),
+                "quantize_per_tensor: scale override must be positive");
+
+    DeviceGuard dg(d.device);
+    auto* L = new fqg_layer_s();
+    try {
+        L->device = d.device;
+        L->bits = d.bits;
+        L->a_fmt = d.a_format;
+        L->b_fmt = d.b_format;
+        L->scale_mode = d.scale_mode;
+        L->k = d.k;
+        L->n = d.n;
+        L->n_total = n_total;
+        L->n_begin = d.n_begin;
+        L->t_x = d.t_x;
+        L->t_w = d.t_w;
+        L->act_scale = d.act_scale;
+        L->qmax = static_cast<double>((1 << (d.bits - 1)) - 1);
+        const Plan px = plan_from_ext(d.t_x, d.ext_x, d.k, d.block_x);
+        const Plan pw = plan_from_ext(d.t_w, d.ext_w, px.padded, d.block_w);
+        L->c1 = px.padded;
+        L->kp = pw.padded;
+        const GatherMaps g = compile_maps(px, pw);
+        require(L->kp * 127ll * 127ll < (1ll << 31), "layer: K' too large for exact INT32");
+        for (int64_t j = 0; j < d.k; ++j)
+            require(d.smooth_scales[j] != 0.0 && std::isfinite(d.smooth_scales[j]),
+                    "layer: smoothing scales must be finite and non-zero");
+        upload(L->d_s, std::vector<double>(d.smooth_scales, d.smooth_scales + d.k));
+        upload(L->d_cap, g.cap_x);
+        upload(L->d_amap, g.amap);
+
+        const bool pack4 = d.b_format == FQG_I4;
+        L->ldb = pack4 ? L->kp / 2 : L->kp;
+        L->d_wq.alloc(static_cast<size_t>(L->n * L->ldb));
+        if (d.weight_q) {
+            require(d.w_scale > 0.0 && std::isfinite(d.w_scale), "layer: w_scale must be > 0");
+            L->w_scale = d.w_scale;
+            const auto packed = pack_weight_q(d.weight_q, L->kp, n_total, d.n_begin, d.n,
+                                              static_cast<int>(L->qmax), pack4, L->ldb);
+            FQG_CUDA(cudaMemcpy(L->d_wq.p, packed.data(), packed.size(), cudaMemcpyHostToDevice));
+        } else {
+            // Offline weight tail of quantize_layer on the device (K3).
+            require(d.t_w > 0.0 && std::isfinite(d.t_w), "layer: t_w must be > 0");
+            DevBuf w, wmap, wcap, capw, scratch;
+            const size_t wbytes = static_cast<size_t>(d.k * n_total) * sizeof(double);
+            w.alloc(wbytes);
+            FQG_CUDA(cudaMemcpy(w.p, d.weight, wbytes, cudaMemcpyHostToDevice));
+            upload(wmap, g.wmap);
+            upload(wcap, g.wcap);
+            upload(capw, g.capw_src);
+            scratch.alloc(16);
+            FQG_CUDA(cudaMemset(scratch.p, 0, 16));
+            auto* amax = scratch.as<unsigned long long>();
+            auto* over = reinterpret_cast<unsigned int*>(amax + 1);
+            weight_absmax(w.as<double>(), d.k, n_total, L->d_s.as<double>(), capw.as<int32_t>(),
+                          d.t_w, amax, over, num_sms(d.device), 0);
+            unsigned long long host[2] = {0, 0};
+            FQG_CUDA(cudaMemcpy(host, scratch.p, 16, cudaMemcpyDeviceToHost));
+            if (static_cast<unsigned int>(host[1]) != 0)
+                throw Error(FQG_ERR_RUNTIME,
+                            "flatten_rows: value exceeds plan capacity (plan built from "
+                            "different statistics)");
+            double wmax;
+            std::memcpy(&wmax, &host[0], 8);
+            if (wmax == 0.0) throw Error(FQG_ERR_RUNTIME, "quantize_layer: weight is all zero");
+            L->w_scale = wmax / L->qmax;  // pipeline.cpp:139-143
+            weight_quant(w.as<double>(), n_total, d.n_begin, d.n, L->d_s.as<double>(),
+                         wmap.as<int32_t>(), wcap.as<int32_t>(), L->kp, d.t_w, L->w_scale,
+                         L->qmax, pack4, L->d_wq.as<uint8_t>(), L->ldb, 0);
+            FQG_CUDA(cudaDeviceSynchronize());
+        }
+        const double sc[2] = {d.scale_mode == FQG_SCALE_STATIC ? d.act_scale : 0.0, L->w_scale};
+        L->d_scale.alloc(sizeof(sc));
+        FQG_CUDA(cudaMemcpy(L->d_scale.p, sc, sizeof(sc), cudaMemcpyHostToDevice));
+        return L;
+    } catch (...) {
+        delete L;
+        throw;
+    }
+}
+
+int64_t ldq_of(const fqg_layer_s* L) { return L->a_fmt == FQG_I4 ? L->kp / 2 : L->kp; }
+
+// Per-call device scratch: q operand, and in dynamic mode {s_x, s_w, amax}.
+struct CallScratch {
+    void* q = nullptr;
+    double* scale = nullptr;
+    unsigned long long* amax = nullptr;
+    cudaStream_t st;
+    ~CallScratch() {
+        if (q) cudaFreeAsync(q, st);
+        if (scale) cudaFreeAsync(scale, st);
+    }
+};
+
+void quantize_acts(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, void* q,
+                   double* scale, unsigned long long* amax, unsigned long long* sat,
+                   cudaStream_t st) {
+    FlattenArgs a{};
+    a.x = x;
+    a.x_dtype = x_dtype;
+    a.ldx = L->k;
+    a.m = m;
+    a.k = L->k;
+    a.kp = L->kp;
+    a.s = L->d_s.as<double>();
+    a.cap = L->d_cap.as<int32_t>();
+    a.amap = L->d_amap.as<int32_t>();
+    a.t = L->t_x;
+    a.scale = scale;
+    a.amax = amax;
+    a.qmax = L->qmax;
+    a.pack4 = L->a_fmt == FQG_I4;
+    a.q = static_cast<uint8_t*>(q);
+    a.ldq = ldq_of(L);
+    a.sat = sat;
+    a.num_sms = num_sms(L->device);
+    flatten_quant(a, st);
+}
+
+void run_gemm(const fqg_layer_s* L, const void* q, int64_t m, void* y, int y_dtype, int64_t ldy,
+              const double* scale, const void* bias, int bias_dtype, cudaStream_t st) {
+    GemmArgs g{q, L->a_fmt, ldq_of(L), L->d_wq.p, L->b_fmt, L->ldb, m, L->n, L->kp,
+               y, y_dtype, ldy, scale, bias, bias ? bias_dtype : FQG_NONE};
+    gemm_i8(g, st);
+}
+
+void forward(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, void* y, int y_dtype,
+             int64_t ldy, const void* bias, int bias_dtype, unsigned long long* sat,
+             cudaStream_t st) {
+    require(m >= 1, "run_layer: empty input");
+    require(x != nullptr && y != nullptr, "run_layer: null buffer");
+    require(ldy >= L->n, "run_layer: ldy < n");
+    CallScratch cs;
+    cs.st = st;
+    FQG_CUDA(cudaMallocAsync(&cs.q, static_cast<size_t>(m * ldq_of(L)), st));
+    const double* scale = L->d_scale.as<double>();
+    double* kscale = L->d_scale.as<double>();
+    if (L->scale_mode == FQG_SCALE_DYNAMIC) {
+        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cs.scale), 32, st));
+        cs.amax = reinterpret_cast<unsigned long long*>(cs.scale + 2);
+        FQG_CUDA(cudaMemcpyAsync(cs.scale, L->d_scale.p, 16, cudaMemcpyDeviceToDevice, st));
+        FQG_CUDA(cudaMemsetAsync(cs.amax, 0, 8, st));
+        scale = kscale = cs.scale;
+    }
+    quantize_acts(L, x, x_dtype, m, cs.q, kscale, cs.amax, sat, st);
+    run_gemm(L, cs.q, m, y, y_dtype, ldy, scale, bias, bias_dtype, st);
+}
+
+}  // namespace
+}  // namespace fqg
+
+using namespace fqg;
+
+extern "C" {
+
+int fqg_layer_create(const fqg_layer_desc* desc, fqg_layer_t* out) {
+    return guard([&] {
+        require(desc && out, "fqg_layer_create: null argument");
+        *out = create(*desc);
+    });
+}
+
+int fqg_layer_destroy(fqg_layer_t layer) {
+    return guard([&] {
+        if (!layer) return;
+        DeviceGuard dg(layer->device);
+        delete layer;
+    });
+}
+
+int fqg_layer_get_info(fqg_layer_t L, fqg_layer_info* i) {
+    return guard([&] {
+        require(L && i, "fqg_layer_get_info: null argument");
+        *i = {L->bits,  L->a_fmt, L->b_fmt,  L->scale_mode, L->k,     L->n,
+              L->c1,    L->kp,    L->n_total, L->n_begin,   L->t_x,   L->t_w,
+              L->act_scale, L->w_scale, L->n * L->ldb};
+    });
+}
+
+int fqg_layer_weight_q(fqg_layer_t L, int32_t* wq, double* w_scale) {
+    return guard([&] {
+        require(L != nullptr, "fqg_layer_weight_q: null layer");
+        DeviceGuard dg(L->device);
+        std::vector<uint8_t> packed(static_cast<size_t>(L->n * L->ldb));
+        FQG_CUDA(cudaMemcpy(packed.data(), L->d_wq.p, packed.size(), cudaMemcpyDeviceToHost));
+        if (wq) {
+            for (int64_t c = 0; c < L->n; ++c)
+                for (int64_t kq = 0; kq < L->kp; ++kq) {
+                    int v;
+                    if (L->b_fmt == FQG_I4) {
+                        const int nib = (packed[c * L->ldb + kq / 2] >> ((kq & 1) * 4)) & 0xF;
+                        v = nib >= 8 ? nib - 16 : nib;
+                    } else {
+                        v = static_cast<int8_t>(packed[c * L->ldb + kq]);
+                    }
+                    wq[kq * L->n + c] = v;
+                }
+        }
+        if (w_scale) *w_scale = L->w_scale;
+    });
+}
+
+int fqg_layer_forward(fqg_layer_t L, const void* x, int x_dtype, int64_t m, void* y, int y_dtype,
+                      int64_t ldy, const void* bias, int bias_dtype,
+                      unsigned long long* saturation_dev, void* stream) {
+    return guard([&] {
+        require(L != nullptr, "run_layer: null layer");
+        DeviceGuard dg(L->device);
+        forward(L, x, x_dtype, m, y, y_dtype, ldy, bias, bias_dtype, saturation_dev,
+                static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fqg_layer_quantize_acts(fqg_layer_t L, const void* x, int x_dtype, int64_t m, void* q,
+                            unsigned long long* saturation_dev, void* stream) {
+    return guard([&] {
+        require(L != nullptr && x && q && m >= 1, "quantize_acts: bad argument");
+        require(L->scale_mode == FQG_SCALE_STATIC,
+                "quantize_acts: the split entry points take the static scale");
+        DeviceGuard dg(L->device);
+        quantize_acts(L, x, x_dtype, m, q, L->d_scale.as<double>(), nullptr, saturation_dev,
+                      static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fqg_layer_gemm(fqg_layer_t L, const void* q, int64_t m, void* y, int y_dtype, int64_t ldy,
+                   const void* bias, int bias_dtype, void* stream) {
+    return guard([&] {
+        require(L != nullptr && q && y && m >= 1, "layer_gemm: bad argument");
+        require(ldy >= L->n, "layer_gemm: ldy < n");
+        DeviceGuard dg(L->device);
+        run_gemm(L, q, m, y, y_dtype, ldy, L->d_scale.as<double>(), bias, bias_dtype,
+                 static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fqg_layer_run_host(fqg_layer_t L, const double* x_host, int64_t m, double* y_host,
+                       int64_t* saturation) {
+    return guard([&] {
+        require(L != nullptr && x_host && y_host, "run_layer: null argument");
+        require(m >= 1, "run_layer: empty input");
+        DeviceGuard dg(L->device);
+        cudaStream_t st = cudaStreamPerThread;
+        void *dx = nullptr, *dy = nullptr;
+        unsigned long long* dsat = nullptr;
+        const size_t xb = static_cast<size_t>(m * L->k) * 8, yb = static_cast<size_t>(m * L->n) * 8;
+        FQG_CUDA(cudaMallocAsync(&dx, xb, st));
+        FQG_CUDA(cudaMallocAsync(&dy, yb, st));
+        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dsat), 8, st));
+        struct Free {
+            void *a, *b, *c;
+            cudaStream_t s;
+            ~Free() {
+                cudaFreeAsync(a, s);
+                cudaFreeAsync(b, s);
+                cudaFreeAsync(c, s);
+                cudaStreamSynchronize(s);
+            }
+        } fr{dx, dy, dsat, st};
+        FQG_CUDA(cudaMemsetAsync(dsat, 0, 8, st));
+        FQG_CUDA(cudaMemcpyAsync(dx, x_host, xb, cudaMemcpyHostToDevice, st));
+        forward(L, dx, FQG_F64, m, dy, FQG_F64, L->n, nullptr, FQG_NONE, dsat, st);
+        unsigned long long sat = 0;
+        FQG_CUDA(cudaMemcpyAsync(y_host, dy, yb, cudaMemcpyDeviceToHost, st));
+        FQG_CUDA(cudaMemcpyAsync(&sat, dsat, 8, cudaMemcpyDeviceToHost, st));
+        FQG_CUDA(cudaStreamSynchronize(st));
+        if (saturation) *saturation = static_cast<int64_t>(sat);
+    });
+}
+
+}  // extern "C"
