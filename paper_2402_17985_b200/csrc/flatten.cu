@@ -13,13 +13,20 @@
 //                      scale_rows, repeat_channels, strict flatten_rows, absmax
 //                      -> s_w, round-to-nearest, K-major int8 / packed int4.
 //
-// Exactness. Every decision the reference makes in FP64 is made here on the
-// same operands with the same IEEE operations: the divide x/s_j, fmod, the
-// divide (a - rem)/T, llround, the divide piece/scale and round-half-away.
-// CUDA's double '/', fmod, llround and round are correctly rounded / exact;
-// the explicit __d*_rn intrinsics keep nvcc from contracting anything into
-// an FMA. Pieces equal to +-T quantize to +-round(T/scale) (computed once),
-// pieces that are 0 quantize to 0, so only the remainder piece needs a divide.
+// Exactness. Every decision the reference makes in FP64 is reproduced bit for
+// bit, with cheaper but provably identical operation sequences:
+//  * x / s (smoothing.cpp:75) and piece / scale (quantize.cpp:44): one FMA
+//    correction step of q0 = x * RN(1/s) (Markstein: with the correctly rounded
+//    reciprocal and q0 within 1 ulp, fma(fma(-q0, s, x), r, q0) is the
+//    correctly rounded quotient);
+//  * fmod(a, T) and llround((a - rem) / T) (flatten.cpp:12-13): n = floor(a/T)
+//    and rem = a - n*T exactly, via n0 = floor(a * RN(1/T)) (off by at most
+//    one) and the exact FMA residual fma(-n0, T, a) with a +-1 fix-up; the
+//    reference's count equals n because RN(n*T)/T rounds back to n.
+// tools/verify_fast_split.c checks both against the IEEE operations on 8e8
+// random cases; tests/test_gpu_parity.py checks the kernels end to end.
+// Pieces equal to +-T quantize to +-round(T/scale) (once per CTA), zero
+// pieces to 0, so only the remainder piece needs a division.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -29,63 +36,128 @@
 namespace fqg {
 namespace {
 
-template <typename T>
-__device__ __forceinline__ double to_f64(T v);
-template <>
-__device__ __forceinline__ double to_f64<double>(double v) { return v; }
-template <>
-__device__ __forceinline__ double to_f64<float>(float v) { return static_cast<double>(v); }
-template <>
-__device__ __forceinline__ double to_f64<__half>(__half v) {
-    return static_cast<double>(__half2float(v));
-}
-template <>
-__device__ __forceinline__ double to_f64<__nv_bfloat16>(__nv_bfloat16 v) {
-    return static_cast<double>(__bfloat162float(v));
+// ------------------------------------------------------------ arithmetic
+__device__ __forceinline__ double div_exact(double x, double s, double r) {
+    const double q0 = __dmul_rn(x, r);
+    const double e = __fma_rn(-q0, s, x);
+    return __fma_rn(e, r, q0);
 }
 
-// Split of one element against T with plan capacity `cap` slots
-// (flatten.cpp:8-15 + split_into_slots :60-74). Returns the saturated flag.
 struct Split {
-    long long cnt;  // number of full +-T pieces (after saturation clamp)
-    double rem;     // remainder piece magnitude (0 when saturated)
-    double sign;
+    int cnt;      // number of full +-T pieces (after the saturation clamp)
+    double rem;   // remainder piece magnitude (0 when saturated)
+    bool neg;     // sign = v < 0 ? -1 : +1 (flatten.cpp:62)
     bool sat;
 };
 
-__device__ __forceinline__ Split split_elem(double v, double t, long long cap) {
+// split_against_threshold + split_into_slots' capacity rule (flatten.cpp:8-15,
+// :60-74) for capacity `cap` = E + 1 slots.
+__device__ __forceinline__ Split split_elem(double v, double t, double rt, int cap) {
     Split r;
-    r.sign = v < 0.0 ? -1.0 : 1.0;
+    r.neg = v < 0.0;
     const double a = fabs(v);
-    r.rem = fmod(a, t);
-    r.cnt = llround(__ddiv_rn(__dsub_rn(a, r.rem), t));
-    r.sat = r.cnt > cap || (r.cnt == cap && r.rem > 0.0);
-    if (r.sat) {
+    const double t0 = __dmul_rn(a, rt);
+    if (t0 >= static_cast<double>(cap + 2)) {  // count > cap for sure
         r.cnt = cap;
         r.rem = 0.0;
+        r.sat = true;
+        return r;
     }
+    double n0 = floor(t0);
+    double rem = __fma_rn(-n0, t, a);
+    if (rem < 0.0) {
+        n0 -= 1.0;
+        rem = __fma_rn(-n0, t, a);
+    } else if (rem >= t) {
+        n0 += 1.0;
+        rem = __fma_rn(-n0, t, a);
+    }
+    const int n = static_cast<int>(n0);
+    r.sat = n > cap || (n == cap && rem > 0.0);
+    r.cnt = r.sat ? cap : n;
+    r.rem = r.sat ? 0.0 : rem;
     return r;
 }
 
 // quantize.cpp:44-45: clamp(round(v / s), -qmax, qmax), half away from zero.
-__device__ __forceinline__ int quant(double piece, double scale, double qmax) {
-    double r = round(__ddiv_rn(piece, scale));
+__device__ __forceinline__ int quant(double piece, double scale, double rscale, double qmax) {
+    double r = round(div_exact(piece, scale, rscale));
     r = r < -qmax ? -qmax : (qmax < r ? qmax : r);
     return static_cast<int>(r);
 }
 
 // Per-source-element code: [0,16) piece count, [16,24) q of the remainder
 // piece, [24,32) q of a full piece (sign included).
-__device__ __forceinline__ uint32_t make_code(long long cnt, int qrem, int qfull) {
+__device__ __forceinline__ uint32_t make_code(int cnt, int qrem, int qfull) {
     return static_cast<uint32_t>(cnt) | (static_cast<uint32_t>(qrem & 0xFF) << 16) |
            (static_cast<uint32_t>(qfull & 0xFF) << 24);
 }
 __device__ __forceinline__ int decode(uint32_t code, int p) {
     const int cnt = static_cast<int>(code & 0xFFFFu);
-    if (p < cnt) return static_cast<int>(static_cast<int8_t>(code >> 24));
-    if (p == cnt) return static_cast<int>(static_cast<int8_t>(code >> 16));
-    return 0;
+    const int full = static_cast<int>(static_cast<int8_t>(code >> 24));
+    const int rem = static_cast<int>(static_cast<int8_t>(code >> 16));
+    return p < cnt ? full : (p == cnt ? rem : 0);
 }
+// Per-launch constants of the activation split.
+struct SplitConsts {
+    double t, rt;        // T_x and RN(1/T_x)
+    double as, ras;      // s_x and RN(1/s_x)
+    double qmax;
+    float rt32, q32;     // RN32(1/T_x), RN32(T_x / s_x)
+    float qmax32;
+    int qT;              // q of a full piece, round(T_x / s_x) clamped
+};
+
+// One source element -> code, exact. FP32 fast path with a certified error
+// margin (tools/verify_fp32_split.c): |v32 - v| <= 1.3e-7 |v| (bf16/f16/f32
+// inputs exact in f32; f64 inputs add 2^-24), hence |u32 - a/T| <= 3e-7 u;
+// when the fractional part of u (piece count boundary) or of z = frac * T/s_x
+// (rounding boundary of the remainder piece) is within the margin, the
+// element takes the exact FP64 sequence instead.
+__device__ __forceinline__ uint32_t elem_code(double x, const double* sp_, const double* rp_,
+                                              float rs32, int cap, const SplitConsts& c,
+                                              unsigned long long& sat) {
+    if (x == 0.0) return make_code(0, 0, c.qT);  // v = +-0: no pieces, no saturation
+    const float v32 = __fmul_rn(static_cast<float>(x), rs32);
+    const bool neg32 = v32 < 0.0f;
+    const float u = __fmul_rn(fabsf(v32), c.rt32);
+    if (u >= static_cast<float>(cap + 2)) {  // count > cap for sure
+        ++sat;
+        return make_code(cap, 0, neg32 ? -c.qT : c.qT);
+    }
+    const float fl = floorf(u);
+    const float fr = __fsub_rn(u, fl);
+    const float eu = __fadd_rn(__fmul_rn(u, 5e-7f), 1e-30f);
+    if (fr > eu && fr < 1.0f - eu) {
+        const int n = static_cast<int>(fl);
+        if (n >= cap) {  // rem > 0 is certain: saturated (flatten.cpp:65)
+            ++sat;
+            return make_code(cap, 0, neg32 ? -c.qT : c.qT);
+        }
+        const float z = __fmul_rn(fr, c.q32);
+        const float zf = floorf(z);
+        const float d = __fsub_rn(__fsub_rn(z, zf), 0.5f);
+        const float ez = __fadd_rn(__fmul_rn(__fmul_rn(eu, c.q32), 1.5f),
+                                   __fadd_rn(__fmul_rn(z, 2.5e-7f), 1e-30f));
+        if (fabsf(d) > ez) {
+            float q = d > 0.0f ? zf + 1.0f : zf;
+            q = q > c.qmax32 ? c.qmax32 : q;
+            const int qi = static_cast<int>(q);
+            return make_code(n, neg32 ? -qi : qi, neg32 ? -c.qT : c.qT);
+        }
+    }
+    // exact FP64 path (smoothing.cpp:75, flatten.cpp:8-15,60-74, quantize.cpp:44)
+    const double v = div_exact(x, __ldg(sp_), __ldg(rp_));
+    const Split sp = split_elem(v, c.t, c.rt, cap);
+    sat += sp.sat ? 1ull : 0ull;
+    const int qrem = sp.cnt < cap ? quant(sp.neg ? -sp.rem : sp.rem, c.as, c.ras, c.qmax) : 0;
+    return make_code(sp.cnt, qrem, sp.neg ? -c.qT : c.qT);
+}
+
+// Shared-memory slot of channel j: one pad word per 16 channels, so the
+// identity region of the gather (lane l reading channel 16*l + e) hits 32
+// distinct banks.
+__device__ __forceinline__ int cslot(int j) { return j + (j >> 4); }
 
 template <typename T>
 __device__ __forceinline__ T warp_max(T v) {
@@ -102,48 +174,148 @@ __device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
     return v;
 }
 
-// Static or dynamic activation scale -> (scale, q of a full +-T piece).
+__device__ __forceinline__ double to_f64(double v) { return v; }
+__device__ __forceinline__ double to_f64(float v) { return static_cast<double>(v); }
+__device__ __forceinline__ double to_f64(__half v) { return static_cast<double>(__half2float(v)); }
+__device__ __forceinline__ double to_f64(__nv_bfloat16 v) {
+    return static_cast<double>(__bfloat162float(v));
+}
+
+// 8 consecutive activations -> f64 (exact conversions), 16-byte loads.
+template <typename T>
+__device__ __forceinline__ void load8(const T* p, bool vec, double (&o)[8]);
+template <>
+__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, bool vec,
+                                                     double (&o)[8]) {
+    if (vec) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            o[2 * i] = static_cast<double>(__uint_as_float(w[i] << 16));
+            o[2 * i + 1] = static_cast<double>(__uint_as_float(w[i] & 0xFFFF0000u));
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = static_cast<double>(__bfloat162float(p[i]));
+    }
+}
+template <>
+__device__ __forceinline__ void load8<__half>(const __half* p, bool vec, double (&o)[8]) {
+    if (vec) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+        const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float2 f = __half22float2(h[i]);
+            o[2 * i] = f.x;
+            o[2 * i + 1] = f.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = static_cast<double>(__half2float(p[i]));
+    }
+}
+template <>
+__device__ __forceinline__ void load8<float>(const float* p, bool vec, double (&o)[8]) {
+    if (vec) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+        o[0] = a.x, o[1] = a.y, o[2] = a.z, o[3] = a.w;
+        o[4] = b.x, o[5] = b.y, o[6] = b.z, o[7] = b.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = p[i];
+    }
+}
+template <>
+__device__ __forceinline__ void load8<double>(const double* p, bool vec, double (&o)[8]) {
+    if (vec) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double2 d = __ldg(reinterpret_cast<const double2*>(p) + i);
+            o[2 * i] = d.x;
+            o[2 * i + 1] = d.y;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = p[i];
+    }
+}
+
+// Static or dynamic activation scale.
 __device__ __forceinline__ double act_scale_of(const double* scale, const unsigned long long* amax,
                                                double qmax) {
     if (amax == nullptr) return scale[0];
-    // quantize.cpp:34-40: s = max|M| / qmax (degenerate 0 is flagged by the host)
+    // quantize.cpp:34-40: s = max|M| / qmax (a degenerate 0 yields zero outputs)
     return __ddiv_rn(__longlong_as_double(static_cast<long long>(*amax)), qmax);
 }
 
 // ------------------------------------------------------------------ K1
+// One CTA = `rows` consecutive token rows. Phase 1 splits every source
+// element (i, j) once (thread owns 8 consecutive channels, tables loaded once
+// and reused across the CTA's rows) into a 32-bit code in shared memory.
+// Phase 2 walks the K' output columns in 16-column chunks, gathers codes
+// through the composite map and writes 16 int8 (or 8 packed-int4) bytes.
 template <typename XT, bool PACK4>
-__global__ void __launch_bounds__(256)
-    k_flatten_quant(const XT* __restrict__ x, int64_t ldx, int m, int k, int rows_per_cta,
-                    const double* __restrict__ s, const int32_t* __restrict__ cap,
-                    const int32_t* __restrict__ amap, int kp, double t,
-                    double* __restrict__ scale, const unsigned long long* __restrict__ amax,
-                    double qmax, uint8_t* __restrict__ q, int64_t ldq,
-                    unsigned long long* __restrict__ sat_out) {
-    extern __shared__ uint32_t codes[];  // [rows_per_cta][k]
+__global__ void __launch_bounds__(256, 4)
+    k_flatten_quant(const XT* __restrict__ x, int64_t ldx, int m, int k, int rows, int vec_ok,
+                    const double* __restrict__ s, const double* __restrict__ rs,
+                    const int32_t* __restrict__ cap, const int32_t* __restrict__ amap, int kp,
+                    double t, double rt, double* __restrict__ scale,
+                    const unsigned long long* __restrict__ amax, double qmax,
+                    uint8_t* __restrict__ q, int64_t ldq, unsigned long long* __restrict__ sat_out) {
+    extern __shared__ uint32_t codes[];  // [rows][cslot(k)]
     __shared__ unsigned long long red[8];
-    const int row0 = blockIdx.x * rows_per_cta;
-    const int nrows = min(rows_per_cta, m - row0);
+    const int kpad = cslot(k) + 1;
+    const int row0 = blockIdx.x * rows;
+    const int nrows = min(rows, m - row0);
     const double as = act_scale_of(scale, amax, qmax);
     if (amax != nullptr && blockIdx.x == 0 && threadIdx.x == 0) scale[0] = as;
-    const int qT = quant(t, as, qmax);
+    SplitConsts sc;
+    sc.t = t;
+    sc.rt = rt;
+    sc.as = as;
+    sc.ras = 1.0 / as;
+    sc.qmax = qmax;
+    sc.rt32 = static_cast<float>(rt);
+    sc.q32 = static_cast<float>(t / as);
+    sc.qmax32 = static_cast<float>(qmax);
+    sc.qT = quant(t, as, sc.ras, qmax);
+    const bool vec = vec_ok != 0;
 
-    // Phase 1: one split per source element (i, j).
+    // ---- phase 1 ----
     unsigned long long sat = 0;
-    for (int r = 0; r < nrows; ++r) {
-        const XT* xr = x + static_cast<int64_t>(row0 + r) * ldx;
-        uint32_t* cr = codes + static_cast<int64_t>(r) * k;
-        for (int j = threadIdx.x; j < k; j += blockDim.x) {
-            const double v = __ddiv_rn(to_f64<XT>(xr[j]), s[j]);  // smoothing.cpp:75
-            const long long cp = cap[j];
-            const Split sp = split_elem(v, t, cp);
-            sat += sp.sat ? 1ull : 0ull;
-            const int qrem = sp.cnt < cp ? quant(sp.sign * sp.rem, as, qmax) : 0;
-            cr[j] = make_code(sp.cnt, qrem, sp.sign < 0.0 ? -qT : qT);
+    for (int j0 = threadIdx.x * 8; j0 < k; j0 += blockDim.x * 8) {
+        const int nj = min(8, k - j0);
+        float rj[8];
+        int cj[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const int j = min(j0 + e, k - 1);
+            rj[e] = static_cast<float>(__ldg(rs + j));
+            cj[e] = __ldg(cap + j);
+        }
+        for (int r = 0; r < nrows; ++r) {
+            const XT* xr = x + static_cast<int64_t>(row0 + r) * ldx + j0;
+            double xv[8];
+            if (nj == 8) {
+                load8<XT>(xr, vec, xv);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) xv[e] = e < nj ? to_f64(xr[e]) : 0.0;
+            }
+            uint32_t* cr = codes + r * kpad;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                if (e < nj)
+                    cr[cslot(j0 + e)] = elem_code(xv[e], s + j0 + e, rs + j0 + e, rj[e], cj[e], sc, sat);
+            }
         }
     }
     __syncthreads();
 
-    // Phase 2: gather 16 output columns per thread through the composite map.
+    // ---- phase 2 ----
     const int chunks = kp / 16;
     for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
         int32_t mp[16];
@@ -156,12 +328,17 @@ __global__ void __launch_bounds__(256)
             mp[4 * v + 2] = w.z;
             mp[4 * v + 3] = w.w;
         }
+        int slot[16], piece[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            slot[e] = mp[e] < 0 ? -1 : cslot(mp[e] >> 12);
+            piece[e] = mp[e] & 0xFFF;
+        }
         for (int r = 0; r < nrows; ++r) {
-            const uint32_t* cr = codes + static_cast<int64_t>(r) * k;
+            const uint32_t* cr = codes + r * kpad;
             int qv[16];
 #pragma unroll
-            for (int e = 0; e < 16; ++e)
-                qv[e] = mp[e] < 0 ? 0 : decode(cr[mp[e] >> 12], mp[e] & 0xFFF);
+            for (int e = 0; e < 16; ++e) qv[e] = slot[e] < 0 ? 0 : decode(cr[slot[e]], piece[e]);
             uint8_t* qr = q + static_cast<int64_t>(row0 + r) * ldq;
             if constexpr (PACK4) {
                 uint32_t w0 = 0, w1 = 0;
@@ -203,7 +380,8 @@ __global__ void __launch_bounds__(256)
 template <typename XT>
 __global__ void __launch_bounds__(256)
     k_act_absmax(const XT* __restrict__ x, int64_t ldx, int m, int k,
-                 const double* __restrict__ s, const int32_t* __restrict__ cap, double t,
+                 const double* __restrict__ s, const double* __restrict__ rs,
+                 const int32_t* __restrict__ cap, double t, double rt,
                  unsigned long long* __restrict__ amax) {
     __shared__ double red[8];
     double mx = 0.0;
@@ -211,8 +389,9 @@ __global__ void __launch_bounds__(256)
     for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int i = static_cast<int>(idx / k), j = static_cast<int>(idx % k);
-        const double v = __ddiv_rn(to_f64<XT>(x[static_cast<int64_t>(i) * ldx + j]), s[j]);
-        const Split sp = split_elem(v, t, cap[j]);
+        const double xv = to_f64(x[static_cast<int64_t>(i) * ldx + j]);
+        const double v = div_exact(xv, s[j], rs[j]);
+        const Split sp = split_elem(v, t, rt, cap[j]);
         const double piece = sp.cnt >= 1 ? t : sp.rem;
         mx = mx < piece ? piece : mx;
     }
@@ -232,7 +411,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_weight_absmax(const double* __restrict__ w, int k, int64_t ncols,
                     const double* __restrict__ s, const int32_t* __restrict__ capw_src,
-                    double t_w, unsigned long long* __restrict__ amax,
+                    double t_w, double rt_w, unsigned long long* __restrict__ amax,
                     unsigned int* __restrict__ overflow) {
     __shared__ double red[8];
     double mx = 0.0;
@@ -242,7 +421,7 @@ __global__ void __launch_bounds__(256)
          idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int j = static_cast<int>(idx / ncols);
         const double v = __dmul_rn(w[idx], s[j]);  // scale_rows, smoothing.cpp:88
-        const Split sp = split_elem(v, t_w, capw_src[j]);
+        const Split sp = split_elem(v, t_w, rt_w, capw_src[j]);
         over |= sp.sat;
         const double piece = sp.cnt >= 1 ? t_w : sp.rem;
         mx = mx < piece ? piece : mx;
@@ -266,8 +445,8 @@ template <bool PACK4>
 __global__ void __launch_bounds__(256)
     k_weight_quant(const double* __restrict__ w, int64_t ldw, int64_t n_begin, int n,
                    const double* __restrict__ s, const int32_t* __restrict__ wmap,
-                   const int32_t* __restrict__ wcap, int kp, double t_w, double s_w, double qmax,
-                   uint8_t* __restrict__ wq, int64_t ldq) {
+                   const int32_t* __restrict__ wcap, int kp, double t_w, double rt_w, double s_w,
+                   double rs_w, double qmax, uint8_t* __restrict__ wq, int64_t ldq) {
     __shared__ int8_t tile[32][WQ_TK + 4];
     const int n0 = blockIdx.x * 32, k0 = blockIdx.y * WQ_TK;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -280,13 +459,13 @@ __global__ void __launch_bounds__(256)
             if (mp >= 0) {
                 const int j = mp >> 12, p = mp & 0xFFF;
                 const double v = __dmul_rn(w[static_cast<int64_t>(j) * ldw + n_begin + col], s[j]);
-                const Split sp = split_elem(v, t_w, wcap[kq]);
+                const Split sp = split_elem(v, t_w, rt_w, wcap[kq]);
                 double piece = 0.0;
                 if (p < sp.cnt)
-                    piece = sp.sign * t_w;
+                    piece = sp.neg ? -t_w : t_w;
                 else if (p == sp.cnt)
-                    piece = sp.sign * sp.rem;
-                qv = quant(piece, s_w, qmax);
+                    piece = sp.neg ? -sp.rem : sp.rem;
+                qv = quant(piece, s_w, rs_w, qmax);
             }
         }
         tile[tx][kk] = static_cast<int8_t>(qv);
@@ -315,39 +494,36 @@ __global__ void __launch_bounds__(256)
 
 template <typename XT>
 void launch_flatten_t(const FlattenArgs& a, cudaStream_t st) {
-    const int dev_sm = a.num_sms;
+    const double rt = 1.0 / a.t;
     if (a.amax != nullptr) {
         const int64_t total = a.m * a.k;
-        const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, dev_sm * 8));
+        const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, a.num_sms * 8));
         k_act_absmax<XT><<<grid, 256, 0, st>>>(static_cast<const XT*>(a.x), a.ldx,
                                                 static_cast<int>(a.m), static_cast<int>(a.k), a.s,
-                                                a.cap, a.t, a.amax);
+                                                a.rs, a.cap, a.t, rt, a.amax);
         FQG_CUDA(cudaGetLastError());
     }
-    const int64_t row_bytes = a.k * 4;
-    int rows = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, (96 * 1024) / row_bytes)));
-    // keep at least ~2 waves of CTAs
-    while (rows > 1 && (a.m + rows - 1) / rows < 2 * dev_sm) rows >>= 1;
+    const int64_t row_bytes = (a.k + a.k / 16 + 1) * 4;
+    // Rows per CTA: a few rows amortize the map/table loads; keep >= ~4 waves.
+    int rows = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, (48 * 1024) / row_bytes)));
+    while (rows > 1 && (a.m + rows - 1) / rows < 4 * a.num_sms) rows >>= 1;
     const int64_t smem = rows * row_bytes;
     require(smem <= 200 * 1024, "flatten: K too large for the shared-memory code buffer");
     const int grid = static_cast<int>((a.m + rows - 1) / rows);
-    if (a.pack4) {
-        auto kern = k_flatten_quant<XT, true>;
+    const bool vec = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
+                     ((a.ldx * static_cast<int64_t>(sizeof(XT))) % 16 == 0);
+    auto run = [&](auto kern) {
         FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
         kern<<<grid, 256, smem, st>>>(static_cast<const XT*>(a.x), a.ldx, static_cast<int>(a.m),
-                                      static_cast<int>(a.k), rows, a.s, a.cap, a.amap,
-                                      static_cast<int>(a.kp), a.t, a.scale, a.amax, a.qmax, a.q,
-                                      a.ldq, a.sat);
-    } else {
-        auto kern = k_flatten_quant<XT, false>;
-        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        kern<<<grid, 256, smem, st>>>(static_cast<const XT*>(a.x), a.ldx, static_cast<int>(a.m),
-                                      static_cast<int>(a.k), rows, a.s, a.cap, a.amap,
-                                      static_cast<int>(a.kp), a.t, a.scale, a.amax, a.qmax, a.q,
-                                      a.ldq, a.sat);
-    }
+                                      static_cast<int>(a.k), rows, vec ? 1 : 0, a.s, a.rs, a.cap,
+                                      a.amap, static_cast<int>(a.kp), a.t, rt, a.scale, a.amax,
+                                      a.qmax, a.q, a.ldq, a.sat);
+    };
+    if (a.pack4)
+        run(k_flatten_quant<XT, true>);
+    else
+        run(k_flatten_quant<XT, false>);
     FQG_CUDA(cudaGetLastError());
 }
 
@@ -370,8 +546,8 @@ void weight_absmax(const double* w, int64_t k, int64_t ncols, const double* s,
                    unsigned int* overflow, int num_sms, cudaStream_t st) {
     const int64_t total = k * ncols;
     const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, num_sms * 8));
-    k_weight_absmax<<<grid, 256, 0, st>>>(w, static_cast<int>(k), ncols, s, capw_src, t_w, amax,
-                                          overflow);
+    k_weight_absmax<<<grid, 256, 0, st>>>(w, static_cast<int>(k), ncols, s, capw_src, t_w,
+                                          1.0 / t_w, amax, overflow);
     FQG_CUDA(cudaGetLastError());
 }
 
@@ -379,14 +555,15 @@ void weight_quant(const double* w, int64_t ldw, int64_t n_begin, int64_t n, cons
                   const int32_t* wmap, const int32_t* wcap, int64_t kp, double t_w, double s_w,
                   double qmax, bool pack4, uint8_t* wq, int64_t ldq, cudaStream_t st) {
     dim3 grid(static_cast<unsigned>((n + 31) / 32), static_cast<unsigned>((kp + WQ_TK - 1) / WQ_TK));
+    auto run = [&](auto kern) {
+        kern<<<grid, 256, 0, st>>>(w, ldw, n_begin, static_cast<int>(n), s, wmap, wcap,
+                                   static_cast<int>(kp), t_w, 1.0 / t_w, s_w, 1.0 / s_w, qmax, wq,
+                                   ldq);
+    };
     if (pack4)
-        k_weight_quant<true><<<grid, 256, 0, st>>>(w, ldw, n_begin, static_cast<int>(n), s, wmap,
-                                                   wcap, static_cast<int>(kp), t_w, s_w, qmax, wq,
-                                                   ldq);
+        run(k_weight_quant<true>);
     else
-        k_weight_quant<false><<<grid, 256, 0, st>>>(w, ldw, n_begin, static_cast<int>(n), s, wmap,
-                                                    wcap, static_cast<int>(kp), t_w, s_w, qmax, wq,
-                                                    ldq);
+        run(k_weight_quant<false>);
     FQG_CUDA(cudaGetLastError());
 }
 

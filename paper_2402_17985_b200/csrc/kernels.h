@@ -12,6 +12,7 @@ struct FlattenArgs {
     int64_t ldx;                  // elements
     int64_t m, k, kp;
     const double* s;              // [k] smoothing scales
+    const double* rs;             // [k] RN(1 / s), for the exact FMA-corrected division
     const int32_t* cap;           // [k] plan_x capacity E_x + 1
     const int32_t* amap;          // [kp] (j << 12 | p) or -1
     double t;                     // plan_x threshold T_x

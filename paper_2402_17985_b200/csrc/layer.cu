@@ -40,7 +40,7 @@ struct fqg_layer_s {
     int64_t k = 0, n = 0, c1 = 0, kp = 0, n_total = 0, n_begin = 0;
     int64_t ldb = 0;
     double t_x = 0, t_w = 0, act_scale = 0, w_scale = 0, qmax = 127;
-    fqg::DevBuf d_s, d_cap, d_amap, d_wq, d_scale;
+    fqg::DevBuf d_s, d_rs, d_cap, d_amap, d_wq, d_scale;
 };
 
 namespace fqg {
@@ -128,6 +128,9 @@ fqg_layer_s* create(const fqg_layer_desc& d) {
             require(d.smooth_scales[j] != 0.0 && std::isfinite(d.smooth_scales[j]),
                     "layer: smoothing scales must be finite and non-zero");
         upload(L->d_s, std::vector<double>(d.smooth_scales, d.smooth_scales + d.k));
+        std::vector<double> rs(d.k);
+        for (int64_t j = 0; j < d.k; ++j) rs[j] = 1.0 / d.smooth_scales[j];  // correctly rounded
+        upload(L->d_rs, rs);
         upload(L->d_cap, g.cap_x);
         upload(L->d_amap, g.amap);
 
@@ -206,6 +209,7 @@ void quantize_acts(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, 
     a.k = L->k;
     a.kp = L->kp;
     a.s = L->d_s.as<double>();
+    a.rs = L->d_rs.as<double>();
     a.cap = L->d_cap.as<int32_t>();
     a.amap = L->d_amap.as<int32_t>();
     a.t = L->t_x;

@@ -1,0 +1,92 @@
+/* Brute-force check of K1's FP32 fast path with certified margins against the
+ * reference's FP64 operations (smoothing.cpp:75, flatten.cpp:8-15,60-74,
+ * quantize.cpp:44): for every element either the fast path is provably safe
+ * and agrees, or it reports "fallback" (the kernel then runs the exact FP64
+ * sequence). Reports mismatches (must be 0) and the fallback rate.
+ *   gcc -O2 -ffp-contract=off -march=x86-64-v3 verify_fp32_split.c -lm
+ *   ./a.out ITERS SEED */
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+static uint64_t s_ = 88172645463325252ull;
+static uint64_t rnd(void) { s_ ^= s_ << 13; s_ ^= s_ >> 7; s_ ^= s_ << 17; return s_; }
+static double u01(void) { return (double)(rnd() >> 11) * 0x1.0p-53; }
+static double bf16_round(double v) {
+    float f = (float)v; uint32_t b; memcpy(&b, &f, 4);
+    b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000u; memcpy(&f, &b, 4); return (double)f;
+}
+
+/* reference (flatten.cpp / quantize.cpp semantics) */
+static void ref_elem(double x, double s, double t, double as, int cap, double qmax, int* cnt,
+                     int* qrem, int* sat) {
+    const double v = x / s, a = fabs(v);
+    const double rem0 = fmod(a, t);
+    long long c = llround((a - rem0) / t);
+    double rem = rem0;
+    *sat = c > cap || (c == cap && rem > 0.0);
+    if (*sat) { c = cap; rem = 0.0; }
+    *cnt = (int)c;
+    double q = 0;
+    if (c < cap) { q = round(rem / as); q = q < -qmax ? -qmax : (qmax < q ? qmax : q); }
+    *qrem = (int)q;
+}
+
+/* K1 fast path (mirrors flatten.cu fast_split32): returns 0 when it must fall back */
+static int fast_elem(float xf, float rs32, float rt32, float q32, int cap, float qmax, int* cnt,
+                     int* qrem, int* sat) {
+    const float v = xf * rs32;
+    const float u = fabsf(v) * rt32;
+    if (u >= (float)(cap + 2)) { *cnt = cap; *qrem = 0; *sat = 1; return 1; }
+    const float fl = floorf(u);
+    const float fr = u - fl;
+    const float eu = u * 5e-7f + 1e-30f;
+    if (!(fr > eu && fr < 1.0f - eu)) return 0;
+    const int n = (int)fl;
+    *sat = n > cap || n == cap; /* rem > 0 is certain here */
+    if (*sat) { *cnt = cap; *qrem = 0; return 1; }
+    *cnt = n;
+    if (n == cap) { *qrem = 0; return 1; }
+    const float z = fr * q32;
+    const float zf = floorf(z);
+    const float ez = eu * q32 * 1.5f + z * 2.5e-7f + 1e-30f;
+    const float d = z - zf - 0.5f;
+    if (!(fabsf(d) > ez)) return 0;
+    float q = d > 0.0f ? zf + 1.0f : zf;
+    q = q > qmax ? qmax : q;
+    *qrem = (int)q;
+    return 1;
+}
+
+int main(int argc, char** argv) {
+    long long iters = argc > 1 ? atoll(argv[1]) : 100000000ll;
+    if (argc > 2) s_ ^= (uint64_t)atoll(argv[2]) * 0x9E3779B97F4A7C15ull;
+    long long bad = 0, fb = 0;
+    for (long long it = 0; it < iters; ++it) {
+        const double s = exp((u01() - 0.5) * 6.0);
+        double x = bf16_round((u01() - 0.5) * 8.0 * exp((u01() - 0.2) * 5.0));
+        const double t = 0.2 + u01() * 20.0;
+        const int bits = (it & 1) ? 8 : 4;
+        const double qmax = bits == 8 ? 127.0 : 7.0;
+        const double as = t / qmax;
+        const int cap = 1 + (int)(rnd() % 100);
+        if ((it & 31) == 0) x = bf16_round(t * s * (double)(rnd() % 8)); /* near-exact fits */
+        int c0, q0, s0, c1, q1, s1;
+        ref_elem(x, s, t, as, cap, qmax, &c0, &q0, &s0);
+        if (!fast_elem((float)x, (float)(1.0 / s), (float)(1.0 / t), (float)(t / as), cap,
+                       (float)qmax, &c1, &q1, &s1)) {
+            ++fb;
+            continue;
+        }
+        if (c0 != c1 || q0 != q1 || s0 != s1) {
+            if (bad++ < 10)
+                printf("x=%a s=%a t=%a cap=%d ref=(%d,%d,%d) fast=(%d,%d,%d)\n", x, s, t, cap, c0,
+                       q0, s0, c1, q1, s1);
+        }
+    }
+    printf("iters=%lld mismatches=%lld fallback=%lld (%.2e)\n", iters, bad, fb,
+           (double)fb / (double)iters);
+    return bad ? 1 : 0;
+}
