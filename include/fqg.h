@@ -39,7 +39,8 @@ typedef enum fqg_dtype {
     FQG_BF16 = 3,
     FQG_I32 = 4, /* raw INT32 accumulators (bit-exact debug dump)          */
     FQG_I8 = 5,  /* int8 operand, one value per byte                       */
-    FQG_I4 = 6,  /* packed int4 operand: byte b = q[2b] & 15 | q[2b+1] << 4 */
+    FQG_I4 = 6,  /* packed int4 operand: per group g of 32 consecutive k,
+                    byte 16g + i = q[32g + i] & 15 | q[32g + 16 + i] << 4 */
     FQG_NONE = 7
 } fqg_dtype;
 

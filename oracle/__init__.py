@@ -133,6 +133,7 @@ class Port:
         L.fqo_repeat_columns.argtypes = [_f64p, I64, I64, _i64p, I64, _f64p]
         L.fqo_quantize_per_tensor.argtypes = [_f64p, I64, C.c_int, F64, _i32p, C.POINTER(F64)]
         L.fqo_int_matmul_raw.argtypes = [_i32p, I64, I64, C.c_int, _i32p, I64, C.c_int, _i64p]
+        L.fqo_accumulator_bound_ok.argtypes = [I64, I64, I64]
         L.fqo_derive_truncation.argtypes = [_f64p, I64, F64, C.c_int, C.POINTER(F64)]
         L.fqo_smoothing_scales.argtypes = [_f64p, _f64p, I64, F64, _f64p]
         L.fqo_collect_channel_maxes.argtypes = [_f64p, I64, I64, I64, _f64p]

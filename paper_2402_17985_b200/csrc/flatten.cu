@@ -86,18 +86,6 @@ __device__ __forceinline__ int quant(double piece, double scale, double rscale, 
     return static_cast<int>(r);
 }
 
-// Per-source-element code: [0,16) piece count, [16,24) q of the remainder
-// piece, [24,32) q of a full piece (sign included).
-__device__ __forceinline__ uint32_t make_code(int cnt, int qrem, int qfull) {
-    return static_cast<uint32_t>(cnt) | (static_cast<uint32_t>(qrem & 0xFF) << 16) |
-           (static_cast<uint32_t>(qfull & 0xFF) << 24);
-}
-__device__ __forceinline__ int decode(uint32_t code, int p) {
-    const int cnt = static_cast<int>(code & 0xFFFFu);
-    const int full = static_cast<int>(static_cast<int8_t>(code >> 24));
-    const int rem = static_cast<int>(static_cast<int8_t>(code >> 16));
-    return p < cnt ? full : (p == cnt ? rem : 0);
-}
 // Per-launch constants of the activation split.
 struct SplitConsts {
     double t, rt;        // T_x and RN(1/T_x)
@@ -107,57 +95,6 @@ struct SplitConsts {
     float qmax32;
     int qT;              // q of a full piece, round(T_x / s_x) clamped
 };
-
-// One source element -> code, exact. FP32 fast path with a certified error
-// margin (tools/verify_fp32_split.c): |v32 - v| <= 1.3e-7 |v| (bf16/f16/f32
-// inputs exact in f32; f64 inputs add 2^-24), hence |u32 - a/T| <= 3e-7 u;
-// when the fractional part of u (piece count boundary) or of z = frac * T/s_x
-// (rounding boundary of the remainder piece) is within the margin, the
-// element takes the exact FP64 sequence instead.
-__device__ __forceinline__ uint32_t elem_code(double x, const double* sp_, const double* rp_,
-                                              float rs32, int cap, const SplitConsts& c,
-                                              unsigned long long& sat) {
-    if (x == 0.0) return make_code(0, 0, c.qT);  // v = +-0: no pieces, no saturation
-    const float v32 = __fmul_rn(static_cast<float>(x), rs32);
-    const bool neg32 = v32 < 0.0f;
-    const float u = __fmul_rn(fabsf(v32), c.rt32);
-    if (u >= static_cast<float>(cap + 2)) {  // count > cap for sure
-        ++sat;
-        return make_code(cap, 0, neg32 ? -c.qT : c.qT);
-    }
-    const float fl = floorf(u);
-    const float fr = __fsub_rn(u, fl);
-    const float eu = __fadd_rn(__fmul_rn(u, 5e-7f), 1e-30f);
-    if (fr > eu && fr < 1.0f - eu) {
-        const int n = static_cast<int>(fl);
-        if (n >= cap) {  // rem > 0 is certain: saturated (flatten.cpp:65)
-            ++sat;
-            return make_code(cap, 0, neg32 ? -c.qT : c.qT);
-        }
-        const float z = __fmul_rn(fr, c.q32);
-        const float zf = floorf(z);
-        const float d = __fsub_rn(__fsub_rn(z, zf), 0.5f);
-        const float ez = __fadd_rn(__fmul_rn(__fmul_rn(eu, c.q32), 1.5f),
-                                   __fadd_rn(__fmul_rn(z, 2.5e-7f), 1e-30f));
-        if (fabsf(d) > ez) {
-            float q = d > 0.0f ? zf + 1.0f : zf;
-            q = q > c.qmax32 ? c.qmax32 : q;
-            const int qi = static_cast<int>(q);
-            return make_code(n, neg32 ? -qi : qi, neg32 ? -c.qT : c.qT);
-        }
-    }
-    // exact FP64 path (smoothing.cpp:75, flatten.cpp:8-15,60-74, quantize.cpp:44)
-    const double v = div_exact(x, __ldg(sp_), __ldg(rp_));
-    const Split sp = split_elem(v, c.t, c.rt, cap);
-    sat += sp.sat ? 1ull : 0ull;
-    const int qrem = sp.cnt < cap ? quant(sp.neg ? -sp.rem : sp.rem, c.as, c.ras, c.qmax) : 0;
-    return make_code(sp.cnt, qrem, sp.neg ? -c.qT : c.qT);
-}
-
-// Shared-memory slot of channel j: one pad word per 16 channels, so the
-// identity region of the gather (lane l reading channel 16*l + e) hits 32
-// distinct banks.
-__device__ __forceinline__ int cslot(int j) { return j + (j >> 4); }
 
 template <typename T>
 __device__ __forceinline__ T warp_max(T v) {
@@ -252,22 +189,118 @@ __device__ __forceinline__ double act_scale_of(const double* scale, const unsign
 }
 
 // ------------------------------------------------------------------ K1
-// One CTA = `rows` consecutive token rows. Phase 1 splits every source
-// element (i, j) once (thread owns 8 consecutive channels, tables loaded once
-// and reused across the CTA's rows) into a 32-bit code in shared memory.
-// Phase 2 walks the K' output columns in 16-column chunks, gathers codes
-// through the composite map and writes 16 int8 (or 8 packed-int4) bytes.
+// FP32 fast path of one element with a certified error margin
+// (tools/verify_fp32_split.c): |v32 - v| <= 1.3e-7 |v| (bf16/f16/f32 inputs
+// are exact in f32; f64 inputs add 2^-24), hence |u32 - a/T| <= 3e-7 u. When
+// the fractional part of u (piece-count boundary) or of z = frac * T/s_x
+// (rounding boundary of the remainder piece) lies within the margin, ok is
+// false and the caller takes the exact FP64 sequence instead.
+struct Fast {
+    int cnt, qrem;
+    bool neg, sat, ok;
+};
+__device__ __forceinline__ Fast fast_elem(float xf, float rs32, int cap, const SplitConsts& c) {
+    Fast o;
+    const float v = __fmul_rn(xf, rs32);
+    o.neg = v < 0.0f;
+    const float u = __fmul_rn(fabsf(v), c.rt32);
+    const bool big = u >= static_cast<float>(cap + 2);
+    const float fl = floorf(u);
+    const float fr = __fsub_rn(u, fl);
+    const float eu = __fadd_rn(__fmul_rn(u, 5e-7f), 1e-30f);
+    const bool okn = fr > eu && fr < 1.0f - eu;
+    const int n = big ? cap : static_cast<int>(fl);
+    const float z = __fmul_rn(fr, c.q32);
+    const float zf = floorf(z);
+    const float d = __fsub_rn(__fsub_rn(z, zf), 0.5f);
+    const float ez = __fadd_rn(__fmul_rn(__fmul_rn(eu, c.q32), 1.5f),
+                               __fadd_rn(__fmul_rn(z, 2.5e-7f), 1e-30f));
+    const bool okz = fabsf(d) > ez;
+    const int qi = static_cast<int>(fminf(d > 0.0f ? zf + 1.0f : zf, c.qmax32));
+    o.sat = big || (okn && n >= cap);
+    o.cnt = o.sat ? cap : n;
+    o.qrem = o.sat ? 0 : (o.neg ? -qi : qi);
+    o.ok = big || (okn && (n >= cap || okz));
+    return o;
+}
+
+// The exact FP64 sequence for one element (smoothing.cpp:75,
+// flatten.cpp:8-15,60-74, quantize.cpp:44): packed cnt | qrem << 16 |
+// neg << 32 | sat << 33. Out of line: it runs for ~0.1% of the elements and
+// keeping it out of the unrolled fast loop keeps that loop in registers.
+__device__ __noinline__ uint64_t slow_elem(double x, const double* sp_, const double* rp_,
+                                           int cap, const SplitConsts& c) {
+    const double v = div_exact(x, __ldg(sp_), __ldg(rp_));
+    const Split sp = split_elem(v, c.t, c.rt, cap);
+    const int qrem = sp.cnt < cap ? quant(sp.neg ? -sp.rem : sp.rem, c.as, c.ras, c.qmax) : 0;
+    return static_cast<uint64_t>(sp.cnt) | (static_cast<uint64_t>(qrem & 0xFFFF) << 16) |
+           (static_cast<uint64_t>(sp.neg) << 32) | (static_cast<uint64_t>(sp.sat) << 33);
+}
+
+// 8 consecutive activations as f32 (exact for bf16/f16/f32) + the f64 value
+// (for non-f64 inputs d = f exactly; the conversion is only needed on the
+// rare exact path).
+template <typename T>
+__device__ __forceinline__ void load8f(const T* p, bool vec, int nj, float (&f)[8],
+                                       double (&d)[8]) {
+    if constexpr (std::is_same<T, __nv_bfloat16>::value) {
+        if (nj == 8 && vec) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+            const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                f[2 * i] = __uint_as_float(w[i] << 16);
+                f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = e < nj ? __bfloat162float(p[e]) : 0.0f;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) d[e] = static_cast<double>(f[e]);
+    } else {
+        if (nj == 8) {
+            load8<T>(p, vec, d);
+        } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) d[e] = e < nj ? to_f64(p[e]) : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = static_cast<float>(d[e]);
+    }
+}
+
+// Packs 32 int8 (k 0..31 of a group) into 16 bytes of the FQG_I4 layout:
+// byte i = q[i] & 15 | q[16 + i] << 4.
+__device__ __forceinline__ uint4 pack_i4(uint4 lo, uint4 hi) {
+    auto p = [](uint32_t a, uint32_t b) {
+        return (a & 0x0F0F0F0Fu) | ((b << 4) & 0xF0F0F0F0u);
+    };
+    return make_uint4(p(lo.x, hi.x), p(lo.y, hi.y), p(lo.z, hi.z), p(lo.w, hi.w));
+}
+
+// One CTA = `rows` consecutive token rows.
+// Phase 1: every source element (i, j) is split once (thread owns 8
+// consecutive channels; tables reused across the CTA's rows) and its
+// quantized pieces are written straight into a shared-memory copy of the
+// plan_x-flattened row (flat[r][0..C1): slot j, extension slots
+// K + off_j + p - 1, zero padding).
+// Phase 2: columns [0, C1) of the final operand ARE the flattened row
+// (repeat_columns keeps column r at r, flatten.cpp:166), copied with 16-byte
+// vectors; columns [C1, K') are plan_w copies of flat columns wsrc[k' - C1],
+// gathered bytewise.
 template <typename XT, bool PACK4>
-__global__ void __launch_bounds__(256, 4)
+__global__ void __launch_bounds__(256, 3)
     k_flatten_quant(const XT* __restrict__ x, int64_t ldx, int m, int k, int rows, int vec_ok,
                     const double* __restrict__ s, const double* __restrict__ rs,
-                    const int32_t* __restrict__ cap, const int32_t* __restrict__ amap, int kp,
-                    double t, double rt, double* __restrict__ scale,
+                    const float* __restrict__ rs32, const int32_t* __restrict__ cap,
+                    const int32_t* __restrict__ off, const int32_t* __restrict__ wsrc, int c1,
+                    int width, int kp, double t, double rt, double* __restrict__ scale,
                     const unsigned long long* __restrict__ amax, double qmax,
                     uint8_t* __restrict__ q, int64_t ldq, unsigned long long* __restrict__ sat_out) {
-    extern __shared__ uint32_t codes[];  // [rows][cslot(k)]
+    extern __shared__ uint4 flat4[];  // [rows][c1] bytes
+    int8_t* flat = reinterpret_cast<int8_t*>(flat4);
     __shared__ unsigned long long red[8];
-    const int kpad = cslot(k) + 1;
     const int row0 = blockIdx.x * rows;
     const int nrows = min(rows, m - row0);
     const double as = act_scale_of(scale, amax, qmax);
@@ -290,73 +323,101 @@ __global__ void __launch_bounds__(256, 4)
         const int nj = min(8, k - j0);
         float rj[8];
         int cj[8];
+        bool any_ext = false;
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int j = min(j0 + e, k - 1);
-            rj[e] = static_cast<float>(__ldg(rs + j));
+            rj[e] = __ldg(rs32 + j);
             cj[e] = __ldg(cap + j);
+            any_ext |= (e < nj) && cj[e] > 1;
         }
         for (int r = 0; r < nrows; ++r) {
-            const XT* xr = x + static_cast<int64_t>(row0 + r) * ldx + j0;
-            double xv[8];
-            if (nj == 8) {
-                load8<XT>(xr, vec, xv);
-            } else {
-#pragma unroll
-                for (int e = 0; e < 8; ++e) xv[e] = e < nj ? to_f64(xr[e]) : 0.0;
-            }
-            uint32_t* cr = codes + r * kpad;
+            float xf[8];
+            double xd[8];
+            load8f<XT>(x + static_cast<int64_t>(row0 + r) * ldx + j0, vec, nj, xf, xd);
+            int8_t* fr = flat + r * c1;
+            uint32_t w0 = 0u, w1 = 0u;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                if (e < nj)
-                    cr[cslot(j0 + e)] = elem_code(xv[e], s + j0 + e, rs + j0 + e, rj[e], cj[e], sc, sat);
+                const Fast f = fast_elem(xf[e], rj[e], cj[e], sc);
+                const bool zero = xd[e] == 0.0;
+                uint64_t res;  // cnt | qrem << 16 | neg << 32 | sat << 33
+                if (zero || f.ok || e >= nj) {
+                    res = zero ? 0ull
+                               : (static_cast<uint64_t>(f.cnt) |
+                                  (static_cast<uint64_t>(f.qrem & 0xFFFF) << 16) |
+                                  (static_cast<uint64_t>(f.neg) << 32) |
+                                  (static_cast<uint64_t>(f.sat) << 33));
+                } else {  // rare: exact FP64 path
+                    res = slow_elem(xd[e], s + j0 + e, rs + j0 + e, cj[e], sc);
+                }
+                const int ce = static_cast<int>(res & 0xFFFF);
+                const int qe = static_cast<int>(static_cast<int16_t>(res >> 16));
+                const int full = (res >> 32) & 1 ? -sc.qT : sc.qT;
+                sat += (e < nj) ? ((res >> 33) & 1) : 0;
+                // slot j = piece 0: a full piece if cnt >= 1, else the remainder.
+                const uint32_t q0 = static_cast<uint32_t>((ce >= 1 ? full : qe) & 0xFF);
+                if (e < 4)
+                    w0 |= q0 << (8 * e);
+                else
+                    w1 |= q0 << (8 * (e - 4));
+                if (any_ext && e < nj && cj[e] > 1) {  // extension slots k + off_j + p - 1
+                    int8_t* dst = fr + k + __ldg(off + j0 + e) - 1;
+                    for (int p = 1; p < cj[e]; ++p)
+                        dst[p] = static_cast<int8_t>(p < ce ? full : (p == ce ? qe : 0));
+                }
+            }
+            if (nj == 8) {
+                *reinterpret_cast<uint2*>(fr + j0) = make_uint2(w0, w1);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e)
+                    if (e < nj) fr[j0 + e] = static_cast<int8_t>((e < 4 ? w0 : w1) >> (8 * (e & 3)));
             }
         }
     }
+    // alignment padding of the flattened row (flatten.cpp:43: zero columns)
+    for (int r = 0; r < nrows; ++r)
+        for (int c = width + threadIdx.x; c < c1; c += blockDim.x) flat[r * c1 + c] = 0;
     __syncthreads();
 
     // ---- phase 2 ----
-    const int chunks = kp / 16;
-    for (int c = threadIdx.x; c < chunks; c += blockDim.x) {
-        int32_t mp[16];
-        const int4* m4 = reinterpret_cast<const int4*>(amap + c * 16);
+    if constexpr (PACK4) {
+        for (int c = threadIdx.x; c < c1 / 32; c += blockDim.x)
+            for (int r = 0; r < nrows; ++r) {
+                const uint4* f4 = reinterpret_cast<const uint4*>(flat + r * c1 + c * 32);
+                *reinterpret_cast<uint4*>(q + static_cast<int64_t>(row0 + r) * ldq + c * 16) =
+                    pack_i4(f4[0], f4[1]);
+            }
+    } else {
+        for (int c = threadIdx.x; c < c1 / 16; c += blockDim.x)
+            for (int r = 0; r < nrows; ++r)
+                *reinterpret_cast<uint4*>(q + static_cast<int64_t>(row0 + r) * ldq + c * 16) =
+                    *reinterpret_cast<const uint4*>(flat + r * c1 + c * 16);
+    }
+    constexpr int G = PACK4 ? 32 : 16;  // output columns per gathered chunk
+    auto gather4 = [](const int8_t* fr, int4 s4) {
+        const int sv[4] = {s4.x, s4.y, s4.z, s4.w};
+        uint32_t acc = 0;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-            const int4 w = __ldg(m4 + v);
-            mp[4 * v] = w.x;
-            mp[4 * v + 1] = w.y;
-            mp[4 * v + 2] = w.z;
-            mp[4 * v + 3] = w.w;
-        }
-        int slot[16], piece[16];
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-            slot[e] = mp[e] < 0 ? -1 : cslot(mp[e] >> 12);
-            piece[e] = mp[e] & 0xFFF;
-        }
+        for (int b = 0; b < 4; ++b)
+            acc |= (sv[b] < 0 ? 0u : static_cast<uint32_t>(static_cast<uint8_t>(fr[sv[b]])))
+                   << (8 * b);
+        return acc;
+    };
+    for (int c = threadIdx.x; c < (kp - c1) / G; c += blockDim.x) {
+        const int4* src4 = reinterpret_cast<const int4*>(wsrc + c * G);
         for (int r = 0; r < nrows; ++r) {
-            const uint32_t* cr = codes + r * kpad;
-            int qv[16];
+            const int8_t* fr = flat + r * c1;
+            uint32_t w[G / 4];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) qv[e] = slot[e] < 0 ? 0 : decode(cr[slot[e]], piece[e]);
+            for (int v = 0; v < G / 4; ++v) w[v] = gather4(fr, __ldg(src4 + v));
             uint8_t* qr = q + static_cast<int64_t>(row0 + r) * ldq;
             if constexpr (PACK4) {
-                uint32_t w0 = 0, w1 = 0;
-#pragma unroll
-                for (int e = 0; e < 8; ++e) w0 |= static_cast<uint32_t>(qv[e] & 0xF) << (4 * e);
-#pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    w1 |= static_cast<uint32_t>(qv[8 + e] & 0xF) << (4 * e);
-                *reinterpret_cast<uint2*>(qr + c * 8) = make_uint2(w0, w1);
+                *reinterpret_cast<uint4*>(qr + (c1 + c * 32) / 2) =
+                    pack_i4(make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]));
             } else {
-                uint32_t w[4];
-#pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    w[v] = (static_cast<uint32_t>(qv[4 * v] & 0xFF)) |
-                           (static_cast<uint32_t>(qv[4 * v + 1] & 0xFF) << 8) |
-                           (static_cast<uint32_t>(qv[4 * v + 2] & 0xFF) << 16) |
-                           (static_cast<uint32_t>(qv[4 * v + 3] & 0xFF) << 24);
-                *reinterpret_cast<uint4*>(qr + c * 16) = make_uint4(w[0], w[1], w[2], w[3]);
+                *reinterpret_cast<uint4*>(qr + c1 + c * 16) = make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
     }
@@ -471,18 +532,26 @@ __global__ void __launch_bounds__(256)
         tile[tx][kk] = static_cast<int8_t>(qv);
     }
     __syncthreads();
-    // Write: each warp writes rows n0+ty, n0+ty+8, ...; lane covers 4 k' values.
+    // Write: each warp writes rows n0+ty, n0+ty+8, ...; lane covers 4 k' values
+    // (int8) or 4 packed bytes (FQG_I4: per 32-k group, byte i = q[i] | q[16+i] << 4).
     for (int r = ty; r < 32; r += 8) {
         const int nn = n0 + r;
         if (nn >= n) continue;
-        const int kk = tx * 4;
-        if (k0 + kk >= kp) continue;
-        const int8_t* src = &tile[r][kk];
         if constexpr (PACK4) {
-            const uint16_t b = static_cast<uint16_t>((src[0] & 0xF) | ((src[1] & 0xF) << 4) |
-                                                     ((src[2] & 0xF) << 8) | ((src[3] & 0xF) << 12));
-            *reinterpret_cast<uint16_t*>(wq + nn * ldq + (k0 + kk) / 2) = b;
+            if (tx >= 16) continue;
+            const int g = tx >> 2, i = (tx & 3) * 4;  // group of 32 k, first byte
+            if (k0 + 32 * g >= kp) continue;
+            const int8_t* lo = &tile[r][32 * g + i];
+            const int8_t* hi = lo + 16;
+            uint32_t b = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                b |= static_cast<uint32_t>((lo[e] & 0xF) | ((hi[e] & 0xF) << 4)) << (8 * e);
+            *reinterpret_cast<uint32_t*>(wq + nn * ldq + k0 / 2 + 16 * g + i) = b;
         } else {
+            const int kk = tx * 4;
+            if (k0 + kk >= kp) continue;
+            const int8_t* src = &tile[r][kk];
             const uint32_t b = static_cast<uint32_t>(static_cast<uint8_t>(src[0])) |
                                (static_cast<uint32_t>(static_cast<uint8_t>(src[1])) << 8) |
                                (static_cast<uint32_t>(static_cast<uint8_t>(src[2])) << 16) |
@@ -503,12 +572,12 @@ void launch_flatten_t(const FlattenArgs& a, cudaStream_t st) {
                                                 a.rs, a.cap, a.t, rt, a.amax);
         FQG_CUDA(cudaGetLastError());
     }
-    const int64_t row_bytes = (a.k + a.k / 16 + 1) * 4;
-    // Rows per CTA: a few rows amortize the map/table loads; keep >= ~4 waves.
-    int rows = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4, (48 * 1024) / row_bytes)));
+    const int64_t row_bytes = a.c1;  // one int8 per flattened column
+    // Rows per CTA: several rows amortize the table/map loads; keep >= ~4 CTAs per SM.
+    int rows = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, (48 * 1024) / row_bytes)));
     while (rows > 1 && (a.m + rows - 1) / rows < 4 * a.num_sms) rows >>= 1;
     const int64_t smem = rows * row_bytes;
-    require(smem <= 200 * 1024, "flatten: K too large for the shared-memory code buffer");
+    require(smem <= 200 * 1024, "flatten: plan_x width too large for the shared-memory row");
     const int grid = static_cast<int>((a.m + rows - 1) / rows);
     const bool vec = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
                      ((a.ldx * static_cast<int64_t>(sizeof(XT))) % 16 == 0);
@@ -516,9 +585,10 @@ void launch_flatten_t(const FlattenArgs& a, cudaStream_t st) {
         FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
         kern<<<grid, 256, smem, st>>>(static_cast<const XT*>(a.x), a.ldx, static_cast<int>(a.m),
-                                      static_cast<int>(a.k), rows, vec ? 1 : 0, a.s, a.rs, a.cap,
-                                      a.amap, static_cast<int>(a.kp), a.t, rt, a.scale, a.amax,
-                                      a.qmax, a.q, a.ldq, a.sat);
+                                      static_cast<int>(a.k), rows, vec ? 1 : 0, a.s, a.rs, a.rs32,
+                                      a.cap, a.off, a.wsrc, static_cast<int>(a.c1),
+                                      static_cast<int>(a.width), static_cast<int>(a.kp), a.t, rt,
+                                      a.scale, a.amax, a.qmax, a.q, a.ldq, a.sat);
     };
     if (a.pack4)
         run(k_flatten_quant<XT, true>);

@@ -59,24 +59,19 @@ struct Layout {
     static constexpr int raw_release = (APK && BPK ? 0 : 1) + unpack_warps;
 };
 
-// 16 packed bytes (32 int4, low nibble = even k) -> 32 int8 in k order.
-// Per nibble v: ((v ^ 8) + 0x78) ^ 0x80 is v sign-extended, with no carry
-// between byte lanes ((v ^ 8) + 0x78 <= 0x87).
+// FQG_I4 layout: per group of 32 k, byte i (0..15) = q[i] & 15 | q[16 + i] << 4.
+// 16 packed bytes -> the group's 32 int8: low nibbles are k 0..15 in order,
+// high nibbles k 16..31. Per nibble v: ((v ^ 8) + 0x78) ^ 0x80 is v
+// sign-extended to 8 bits with no carry between byte lanes ((v ^ 8) + 0x78
+// <= 0x87); the AND and first XOR fuse into one LOP3.
 __device__ __forceinline__ uint32_t sext4x4(uint32_t nib) {
     return ((nib ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
 }
 __device__ __forceinline__ void unpack16(uint4 p, uint4& o0, uint4& o1) {
-    const uint32_t w[4] = {p.x, p.y, p.z, p.w};
-    uint32_t o[8];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint32_t lo = sext4x4(w[i] & 0x0F0F0F0Fu);
-        const uint32_t hi = sext4x4((w[i] >> 4) & 0x0F0F0F0Fu);
-        o[2 * i] = __byte_perm(lo, hi, 0x5140);
-        o[2 * i + 1] = __byte_perm(lo, hi, 0x7362);
-    }
-    o0 = make_uint4(o[0], o[1], o[2], o[3]);
-    o1 = make_uint4(o[4], o[5], o[6], o[7]);
+    o0 = make_uint4(sext4x4(p.x & 0x0F0F0F0Fu), sext4x4(p.y & 0x0F0F0F0Fu),
+                    sext4x4(p.z & 0x0F0F0F0Fu), sext4x4(p.w & 0x0F0F0F0Fu));
+    o1 = make_uint4(sext4x4((p.x >> 4) & 0x0F0F0F0Fu), sext4x4((p.y >> 4) & 0x0F0F0F0Fu),
+                    sext4x4((p.z >> 4) & 0x0F0F0F0Fu), sext4x4((p.w >> 4) & 0x0F0F0F0Fu));
 }
 
 // Expand `rows` x 64 packed bytes (plain rows) into rows x 128 int8 in the

@@ -93,10 +93,16 @@ GatherMaps compile_maps(const Plan& px, const Plan& pw) {
     g.wmap.assign(g.kp, -1);
     g.wcap.assign(g.kp, 1);
     g.cap_x.resize(k);
+    g.off_x.resize(k);
     g.capw_src.resize(k);
+    g.c1 = px.padded;
+    g.width_x = k + px.c_extend;
+    g.wsrc.assign(g.kp - px.padded, -1);
+    for (int64_t kq = px.padded; kq < g.kp; ++kq) g.wsrc[kq - px.padded] = static_cast<int32_t>(sw[kq]);
     for (int64_t j = 0; j < k; ++j) {
         require(px.ext[j] + 1 <= kMaxPieces, "plan_x: a channel has more than 4095 extensions");
         g.cap_x[j] = static_cast<int32_t>(px.ext[j] + 1);
+        g.off_x[j] = static_cast<int32_t>(px.off[j]);
         // Every copy row of source row j carries row j's maximum, hence the
         // same plan_w extension count (repeat_channels, flatten.cpp:136-152).
         g.capw_src[j] = static_cast<int32_t>(pw.ext[j] + 1);

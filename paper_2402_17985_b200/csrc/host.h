@@ -9,6 +9,11 @@ namespace fqg {
 
 constexpr int64_t kMaxPieces = 4095;  // piece index is stored in 12 bits of a map entry
 
+// FQG_I4 packing: per group of 32 consecutive k, byte i (0..15) holds k = 32g + i
+// in its low nibble and k = 32g + 16 + i in its high nibble.
+inline int64_t i4_byte(int64_t k) { return (k >> 5) * 16 + (k & 15); }
+inline int i4_shift(int64_t k) { return (k & 16) ? 4 : 0; }
+
 struct SlotSplit {
     int64_t count = 0;
     double rem = 0.0;
@@ -34,7 +39,12 @@ struct GatherMaps {
     int64_t kp = 0;
     std::vector<int32_t> amap, wmap, wcap;
     std::vector<int32_t> cap_x;     // [K] plan_x capacity E_x + 1
+    std::vector<int32_t> off_x;     // [K] plan_x ext_offset
     std::vector<int32_t> capw_src;  // [K] plan_w capacity of source row j
+    // Final columns [C1, K') are plan_w extension copies of flattened columns:
+    // wsrc[k' - C1] = r, or -1 for plan_w alignment padding.
+    std::vector<int32_t> wsrc;
+    int64_t c1 = 0, width_x = 0;
 };
 GatherMaps compile_maps(const Plan& px, const Plan& pw);
 

@@ -40,7 +40,8 @@ struct fqg_layer_s {
     int64_t k = 0, n = 0, c1 = 0, kp = 0, n_total = 0, n_begin = 0;
     int64_t ldb = 0;
     double t_x = 0, t_w = 0, act_scale = 0, w_scale = 0, qmax = 127;
-    fqg::DevBuf d_s, d_rs, d_cap, d_amap, d_wq, d_scale;
+    int64_t width_x = 0;
+    fqg::DevBuf d_s, d_rs, d_rs32, d_cap, d_off, d_wsrc, d_amap, d_wq, d_scale;
 };
 
 namespace fqg {
@@ -74,8 +75,8 @@ std::vector<uint8_t> pack_weight_q(const int32_t* wq, int64_t kp, int64_t n_tota
             const int32_t v = row[c];
             require(v >= -qmax && v <= qmax, "weight_q value outside [-qmax, qmax]");
             if (pack4) {
-                uint8_t& b = out[c * ldb + kq / 2];
-                b |= static_cast<uint8_t>((v & 0xF) << ((kq & 1) * 4));
+                uint8_t& b = out[c * ldb + i4_byte(kq)];
+                b |= static_cast<uint8_t>((v & 0xF) << i4_shift(kq));
             } else {
                 out[c * ldb + kq] = static_cast<uint8_t>(static_cast<int8_t>(v));
             }
@@ -129,10 +130,18 @@ fqg_layer_s* create(const fqg_layer_desc& d) {
                     "layer: smoothing scales must be finite and non-zero");
         upload(L->d_s, std::vector<double>(d.smooth_scales, d.smooth_scales + d.k));
         std::vector<double> rs(d.k);
-        for (int64_t j = 0; j < d.k; ++j) rs[j] = 1.0 / d.smooth_scales[j];  // correctly rounded
+        std::vector<float> rs32(d.k);
+        for (int64_t j = 0; j < d.k; ++j) {
+            rs[j] = 1.0 / d.smooth_scales[j];  // correctly rounded
+            rs32[j] = static_cast<float>(rs[j]);
+        }
         upload(L->d_rs, rs);
+        upload(L->d_rs32, rs32);
         upload(L->d_cap, g.cap_x);
+        upload(L->d_off, g.off_x);
+        upload(L->d_wsrc, g.wsrc);
         upload(L->d_amap, g.amap);
+        L->width_x = g.width_x;
 
         const bool pack4 = d.b_format == FQG_I4;
         L->ldb = pack4 ? L->kp / 2 : L->kp;
@@ -210,8 +219,13 @@ void quantize_acts(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, 
     a.kp = L->kp;
     a.s = L->d_s.as<double>();
     a.rs = L->d_rs.as<double>();
+    a.rs32 = L->d_rs32.as<float>();
     a.cap = L->d_cap.as<int32_t>();
+    a.off = L->d_off.as<int32_t>();
+    a.wsrc = L->d_wsrc.as<int32_t>();
     a.amap = L->d_amap.as<int32_t>();
+    a.c1 = L->c1;
+    a.width = L->width_x;
     a.t = L->t_x;
     a.scale = scale;
     a.amax = amax;
@@ -295,7 +309,7 @@ int fqg_layer_weight_q(fqg_layer_t L, int32_t* wq, double* w_scale) {
                 for (int64_t kq = 0; kq < L->kp; ++kq) {
                     int v;
                     if (L->b_fmt == FQG_I4) {
-                        const int nib = (packed[c * L->ldb + kq / 2] >> ((kq & 1) * 4)) & 0xF;
+                        const int nib = (packed[c * L->ldb + i4_byte(kq)] >> i4_shift(kq)) & 0xF;
                         v = nib >= 8 ? nib - 16 : nib;
                     } else {
                         v = static_cast<int8_t>(packed[c * L->ldb + kq]);

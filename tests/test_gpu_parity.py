@@ -33,10 +33,11 @@ def make_case(port, fq, k, n, m, bits, index=0, rows=32, samples=4, **synth):
 
 
 def unpack_i4(packed: np.ndarray) -> np.ndarray:
+    """FQG_I4: per group of 32 k, byte i = q[i] & 15 | q[16 + i] << 4."""
     p = packed.view(np.uint8).astype(np.int32)
-    lo, hi = p & 15, p >> 4
-    out = np.empty((p.shape[0], p.shape[1] * 2), np.int32)
-    out[:, 0::2], out[:, 1::2] = lo, hi
+    rows, nbytes = p.shape
+    g = p.reshape(rows, nbytes // 16, 16)
+    out = np.concatenate([g & 15, g >> 4], axis=2).reshape(rows, nbytes * 2)
     return np.where(out >= 8, out - 16, out)
 
 
