@@ -294,12 +294,14 @@ __global__ void __launch_bounds__(256, 3)
     k_flatten_quant(const XT* __restrict__ x, int64_t ldx, int m, int k, int rows, int vec_ok,
                     const double* __restrict__ s, const double* __restrict__ rs,
                     const float* __restrict__ rs32, const int32_t* __restrict__ cap,
-                    const int32_t* __restrict__ off, const int32_t* __restrict__ wsrc, int c1,
-                    int width, int kp, double t, double rt, double* __restrict__ scale,
+                    const int32_t* __restrict__ ecomp, const int32_t* __restrict__ xsrc,
+                    int n_ext, const int32_t* __restrict__ wsrc, int c1, int width, int kp,
+                    double t, double rt, double* __restrict__ scale,
                     const unsigned long long* __restrict__ amax, double qmax,
                     uint8_t* __restrict__ q, int64_t ldq, unsigned long long* __restrict__ sat_out) {
-    extern __shared__ uint4 flat4[];  // [rows][c1] bytes
+    extern __shared__ uint4 flat4[];  // [rows][c1] bytes, then [rows][n_ext] codes
     int8_t* flat = reinterpret_cast<int8_t*>(flat4);
+    uint32_t* codes = reinterpret_cast<uint32_t*>(flat + rows * c1);
     __shared__ unsigned long long red[8];
     const int row0 = blockIdx.x * rows;
     const int nrows = min(rows, m - row0);
@@ -361,11 +363,10 @@ __global__ void __launch_bounds__(256, 3)
                     w0 |= q0 << (8 * e);
                 else
                     w1 |= q0 << (8 * (e - 4));
-                if (any_ext && e < nj && cj[e] > 1) {  // extension slots k + off_j + p - 1
-                    int8_t* dst = fr + k + __ldg(off + j0 + e) - 1;
-                    for (int p = 1; p < cj[e]; ++p)
-                        dst[p] = static_cast<int8_t>(p < ce ? full : (p == ce ? qe : 0));
-                }
+                if (any_ext && e < nj && cj[e] > 1)  // channel with extension slots
+                    codes[r * n_ext + __ldg(ecomp + j0 + e)] =
+                        static_cast<uint32_t>(ce) | (static_cast<uint32_t>(qe & 0xFF) << 16) |
+                        (static_cast<uint32_t>((res >> 32) & 1) << 24);
             }
             if (nj == 8) {
                 *reinterpret_cast<uint2*>(fr + j0) = make_uint2(w0, w1);
@@ -376,9 +377,25 @@ __global__ void __launch_bounds__(256, 3)
             }
         }
     }
-    // alignment padding of the flattened row (flatten.cpp:43: zero columns)
-    for (int r = 0; r < nrows; ++r)
-        for (int c = width + threadIdx.x; c < c1; c += blockDim.x) flat[r * c1 + c] = 0;
+    __syncthreads();
+    // ---- phase 1b: extension slots [K, width) (piece p of channel j at
+    // K + off_j + p - 1, flatten.cpp:86-88) in parallel, and the alignment
+    // padding [width, C1) (zeros, flatten.cpp:43) ----
+    for (int r = 0; r < nrows; ++r) {
+        int8_t* fr = flat + r * c1;
+        const uint32_t* cr = codes + r * n_ext;
+        for (int i = threadIdx.x; i < c1 - k; i += blockDim.x) {
+            int v = 0;
+            if (k + i < width) {
+                const int xs = __ldg(xsrc + i);
+                const uint32_t code = cr[xs >> 12];
+                const int p = xs & 0xFFF, cnt = static_cast<int>(code & 0xFFFFu);
+                const int full = (code >> 24) & 1 ? -sc.qT : sc.qT;
+                v = p < cnt ? full : (p == cnt ? static_cast<int>(static_cast<int8_t>(code >> 16)) : 0);
+            }
+            fr[k + i] = static_cast<int8_t>(v);
+        }
+    }
     __syncthreads();
 
     // ---- phase 2 ----
@@ -572,7 +589,7 @@ void launch_flatten_t(const FlattenArgs& a, cudaStream_t st) {
                                                 a.rs, a.cap, a.t, rt, a.amax);
         FQG_CUDA(cudaGetLastError());
     }
-    const int64_t row_bytes = a.c1;  // one int8 per flattened column
+    const int64_t row_bytes = a.c1 + 4 * a.n_ext;  // flattened row + extension-channel codes
     // Rows per CTA: several rows amortize the table/map loads; keep >= ~4 CTAs per SM.
     int rows = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, (48 * 1024) / row_bytes)));
     while (rows > 1 && (a.m + rows - 1) / rows < 4 * a.num_sms) rows >>= 1;
@@ -586,8 +603,9 @@ void launch_flatten_t(const FlattenArgs& a, cudaStream_t st) {
                                       static_cast<int>(smem)));
         kern<<<grid, 256, smem, st>>>(static_cast<const XT*>(a.x), a.ldx, static_cast<int>(a.m),
                                       static_cast<int>(a.k), rows, vec ? 1 : 0, a.s, a.rs, a.rs32,
-                                      a.cap, a.off, a.wsrc, static_cast<int>(a.c1),
-                                      static_cast<int>(a.width), static_cast<int>(a.kp), a.t, rt,
+                                      a.cap, a.ecomp, a.xsrc, static_cast<int>(a.n_ext), a.wsrc,
+                                      static_cast<int>(a.c1), static_cast<int>(a.width),
+                                      static_cast<int>(a.kp), a.t, rt,
                                       a.scale, a.amax, a.qmax, a.q, a.ldq, a.sat);
     };
     if (a.pack4)

@@ -78,6 +78,7 @@ struct GemmArgs {
     const double* scale;  // device: scale[0] = s_x, scale[1] = s_w
     const void* bias;     // device [N] or nullptr
     int bias_dtype;
+    int variant = 0;      // 0 auto, 1 single-CTA kernel, 2 CTA-pair kernel
 };
 void gemm_i8(const GemmArgs& g, cudaStream_t stream);
 

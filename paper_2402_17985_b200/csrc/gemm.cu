@@ -22,6 +22,8 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "fqg_internal.h"
@@ -346,6 +348,280 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
     }
 }
 
+// Developer instrumentation (FQG_GEMM_DEBUG=1): per-CTA cycles spent in each
+// role's barrier waits. Off by default (one predicated branch per wait).
+__device__ unsigned long long g_dbg[296][8];
+#define FQG_TWAIT(slot, ...)                                                   \
+    do {                                                                       \
+        const long long t0_ = dbg ? clock64() : 0;                             \
+        __VA_ARGS__;                                                           \
+        if (dbg) atomicAdd(&g_dbg[blockIdx.x % 296][slot], clock64() - t0_);   \
+    } while (0)
+
+// ------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
+// 256 x 256 output tile with tcgen05.mma.cta_group::2 (M = 256, N = 256,
+// K = 32). Each CTA stages its own 128 rows of A and 128 of the 256 rows of
+// B, so per SM the smem/L2 operand traffic per MMA drops from 48 KB to 32 KB
+// per 128-deep k-block versus the 1-CTA 128 x 256 tile. The even CTA issues
+// the MMAs; commits multicast to both CTAs' barriers; each CTA's epilogue
+// drains its own TMEM half (its 128 rows x 256 columns).
+//   int8 operands: 2-SM TMA (completion counted on the leader's barrier);
+//   packed int4 operands: 1-SM TMA into this CTA's raw ring, local unpack
+//   warps expand to int8 and signal the leader.
+template <int STAGES, bool APK, bool BPK>
+struct PairLayout {
+    static constexpr int BN = 256;
+    static constexpr bool packed = APK || BPK;
+    static constexpr int a_raw = APK ? BM * BK / 2 : BM * BK;       // own 128 rows of A
+    static constexpr int b_raw = BPK ? (BN / 2) * BK / 2 : (BN / 2) * BK;  // own half of B
+    static constexpr int raw_stage = a_raw + b_raw;
+    static constexpr int direct_bytes = (APK ? 0 : a_raw) + (BPK ? 0 : b_raw);
+    static constexpr int packed_bytes = (APK ? a_raw : 0) + (BPK ? b_raw : 0);
+    static constexpr int USTAGES = packed ? 3 : 0;
+    static constexpr int a_unp = APK ? BM * BK : 0;
+    static constexpr int b_unp = BPK ? (BN / 2) * BK : 0;
+    static constexpr int unp_stage = a_unp + b_unp;
+    static constexpr int unp_off = STAGES * raw_stage;
+    static constexpr int bar_off = unp_off + USTAGES * unp_stage;
+    static constexpr int n_bars = 3 * STAGES + 2 * USTAGES + 4;
+    static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
+    static constexpr int unpack_warps = packed ? 4 : 0;
+    static constexpr int threads = 256 + 32 * unpack_warps;
+    // Arrivals freeing a raw stage in each CTA: the leader's multicast MMA
+    // commit when an operand is read straight from the raw stage, plus one per
+    // local unpack warp.
+    static constexpr int raw_release = (direct_bytes > 0 ? 1 : 0) + unpack_warps;
+};
+
+template <int STAGES, int OUT, bool APK, bool BPK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, APK, BPK>::threads, 1)
+    k_gemm_i8_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
+                   const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
+                   int vec_ok, int dbg) {
+    using L = PairLayout<STAGES, APK, BPK>;
+    const long long t_start = clock64();
+    unsigned long long gstart = 0;
+    if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gstart));
+    constexpr int BN = L::BN;
+    constexpr int U = L::USTAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full_mma = reinterpret_cast<uint64_t*>(smem + L::bar_off);  // leader: direct operands
+    uint64_t* full_unp = full_mma + STAGES;  // own: packed operands landed
+    uint64_t* empty = full_unp + STAGES;     // own: raw stage free
+    uint64_t* ufull = empty + STAGES;        // leader: unpacked stage ready (both CTAs)
+    uint64_t* uempty = ufull + U;            // own: unpacked stage consumed
+    uint64_t* tfull = uempty + U;            // own: accumulator ready
+    uint64_t* tempty = tfull + 2;            // leader: accumulator drained (both CTAs)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int num_m = (m + 2 * BM - 1) / (2 * BM);
+    const int num_n = (n + BN - 1) / BN;
+    const int num_tiles = num_m * num_n;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (threadIdx.x == 0) {
+        ptx::tma_prefetch_desc(&tmA);
+        ptx::tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full_mma[s], 1);
+            ptx::mbar_init(&full_unp[s], 1);
+            ptx::mbar_init(&empty[s], L::raw_release);
+        }
+        for (int u = 0; u < U; ++u) {
+            ptx::mbar_init(&ufull[u], 2 * L::unpack_warps);
+            ptx::mbar_init(&uempty[u], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 8);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc_pair(tmem_holder, 2 * BN);
+        ptx::tmem_relinquish_pair();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer (both CTAs) ----------------
+        const uint64_t keep = ptx::policy_evict_last();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            const int m_blk = tile % num_m, n_blk = tile / num_m;
+            const int a_row = m_blk * 2 * BM + rank * BM;
+            const int b_row = n_blk * BN + rank * (BN / 2);
+            for (int kb = 0; kb < num_kb; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                uint8_t* sa = smem + stage * L::raw_stage;
+                uint8_t* sb = sa + L::a_raw;
+                const uint32_t lead_full = ptx::mapa(ptx::smem_u32(&full_mma[stage]), 0);
+                if constexpr (L::direct_bytes > 0) {
+                    if (leader) ptx::mbar_arrive_expect_tx(&full_mma[stage], 2 * L::direct_bytes);
+                }
+                if constexpr (L::packed_bytes > 0)
+                    ptx::mbar_arrive_expect_tx(&full_unp[stage], L::packed_bytes);
+                if constexpr (APK)
+                    ptx::tma_load_2d_hint(sa, &tmA, &full_unp[stage], kb * BK / 2, a_row, keep);
+                else
+                    ptx::tma_load_2d_2sm(sa, &tmA, lead_full, kb * BK, a_row, keep);
+                if constexpr (BPK)
+                    ptx::tma_load_2d_hint(sb, &tmB, &full_unp[stage], kb * BK / 2, b_row, keep);
+                else
+                    ptx::tma_load_2d_2sm(sb, &tmB, lead_full, kb * BK, b_row, keep);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ---------------- MMA issuer (leader CTA) ----------------
+        constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN);
+        int stage = 0, us = 0;
+        uint32_t phase = 0, uphase = 0;
+        int it = 0;
+        const long long t_mma0 = clock64();
+        unsigned long long g0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+        long long nkb_done = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            FQG_TWAIT(2, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                if constexpr (L::direct_bytes > 0) ptx::mbar_wait(&full_mma[stage], phase);
+                if constexpr (L::packed) ptx::mbar_wait(&ufull[us], uphase);
+                ptx::tc_fence_after();
+                const uint32_t raw = ptx::smem_u32(smem + stage * L::raw_stage);
+                const uint32_t unp = ptx::smem_u32(smem + L::unp_off + us * L::unp_stage);
+                const uint32_t a_addr = APK ? unp : raw;
+                const uint32_t b_addr = BPK ? unp + L::a_unp : raw + L::a_raw;
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k) {
+                    ptx::mma_i8_pair(d_tmem, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
+                                     ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
+                                     (kb | k) != 0 ? 1u : 0u);
+                }
+                if constexpr (L::direct_bytes > 0) ptx::mma_commit_pair(&empty[stage], 0x3);
+                if constexpr (L::packed) {
+                    ptx::mma_commit_pair(&uempty[us], 0x3);
+                    if (++us == U) {
+                        us = 0;
+                        uphase ^= 1;
+                    }
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            ptx::mma_commit_pair(&tfull[acc], 0x3);
+            nkb_done += num_kb;
+        }
+        if (dbg) {
+            atomicAdd(&g_dbg[blockIdx.x % 296][5], clock64() - t_mma0);
+            atomicAdd(&g_dbg[blockIdx.x % 296][6], static_cast<unsigned long long>(nkb_done));
+            atomicAdd(&g_dbg[blockIdx.x % 296][7], t_mma0 - t_start);
+            unsigned long long g1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
+            atomicAdd(&g_dbg[blockIdx.x % 296][4], g1 - g0);  // ns of the MMA loop
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------- epilogue (both CTAs: own 128 rows) ----------------
+        const int ew = warp - 4;
+        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
+        int it = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+            const int m_blk = tile % num_m, n_blk = tile / num_m;
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            unsigned long long ge0 = 0;
+            if (dbg && lane == 0 && ew == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
+            const int row = m_blk * 2 * BM + rank * BM + ew * 32 + lane;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+                ptx::tmem_wait_ld();
+                const int col0 = n_blk * BN + c * 32;
+                if (row < m && col0 < n) {
+                    const int ncols = min(32, n - col0);
+                    store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
+                                         bias_dt, col0, ncols, vec_ok != 0);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+            if (dbg && lane == 0 && ew == 0) {
+                unsigned long long ge1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge1));
+                atomicAdd(&g_dbg[blockIdx.x % 296][1], ge1 - ge0);
+                atomicAdd(&g_dbg[blockIdx.x % 296][2], 1ull);
+            }
+        }
+    } else if (L::packed && warp >= 8) {
+        // ---------------- int4 -> int8 unpack warps (both CTAs) ----------------
+        const int utid = threadIdx.x - 256, nut = 32 * L::unpack_warps;
+        int stage = 0, us = 0;
+        uint32_t phase = 0, uphase = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            for (int kb = 0; kb < num_kb; ++kb) {
+                ptx::mbar_wait(&full_unp[stage], phase);
+                ptx::mbar_wait(&uempty[us], uphase ^ 1);
+                const uint8_t* raw = smem + stage * L::raw_stage;
+                uint8_t* unp = smem + L::unp_off + us * L::unp_stage;
+                if constexpr (APK) unpack_tile(raw, unp, BM, utid, nut);
+                if constexpr (BPK) unpack_tile(raw + L::a_raw, unp + L::a_unp, BN / 2, utid, nut);
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&ufull[us]), 0));
+                    ptx::mbar_arrive(&empty[stage]);
+                }
+                if (++us == U) {
+                    us = 0;
+                    uphase ^= 1;
+                }
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        __syncwarp();
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair(tmem_base, 2 * BN);
+    }
+    if (dbg && threadIdx.x == 32) {
+        unsigned long long gend;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gend));
+        g_dbg[blockIdx.x % 296][0] = gstart;
+        g_dbg[blockIdx.x % 296][3] = gend;
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -392,6 +668,89 @@ void launch(const GemmArgs& g, cudaStream_t stream) {
     FQG_CUDA(cudaGetLastError());
 }
 
+template <int STAGES, int OUT, bool APK, bool BPK>
+void launch_pair(const GemmArgs& g, cudaStream_t stream) {
+    using L = PairLayout<STAGES, APK, BPK>;
+    static_assert(L::total <= 227 * 1024, "shared memory budget");
+    CUtensorMap ta, tb;
+    make_tmap_2d_u8(&ta, g.a, static_cast<uint64_t>(APK ? g.kp / 2 : g.kp),
+                    static_cast<uint64_t>(g.m), static_cast<uint64_t>(g.lda), APK ? BK / 2 : BK,
+                    BM, APK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
+    make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(BPK ? g.kp / 2 : g.kp),
+                    static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.ldb), BPK ? BK / 2 : BK,
+                    L::BN / 2, BPK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
+    auto kern = k_gemm_i8_pair<STAGES, OUT, APK, BPK>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        attr_set = true;
+    }
+    int dev = 0;
+    FQG_CUDA(cudaGetDevice(&dev));
+    const int num_tiles =
+        static_cast<int>(((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n + L::BN - 1) / L::BN));
+    const int clusters = std::max(1, std::min(num_tiles, num_sms(dev) / 2));
+    const int esz = dtype_size(g.y_dtype);
+    const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
+    const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
+    static const int dbg = [] {
+        const char* e = std::getenv("FQG_GEMM_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (dbg) {
+        static unsigned long long zeros[296][8] = {};
+        FQG_CUDA(cudaMemcpyToSymbol(g_dbg, zeros, sizeof(zeros)));
+    }
+    kern<<<2 * clusters, L::threads, L::total, stream>>>(
+        ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb, g.scale, g.bias,
+        g.bias_dtype, vec ? 1 : 0, dbg);
+    FQG_CUDA(cudaGetLastError());
+    if (dbg) {
+        unsigned long long h[296][8];
+        FQG_CUDA(cudaDeviceSynchronize());
+        FQG_CUDA(cudaMemcpyFromSymbol(h, g_dbg, sizeof(h)));
+        double acc[8] = {0};
+        const int nc = 2 * clusters;
+        for (int c = 0; c < nc; ++c)
+            for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(h[c][i]) / nc;
+        // leader-only slots are averaged over both CTAs of a pair: x2
+        std::fprintf(stderr,
+                     "[fqg gemm pair] per leader: mma loop %.0f cyc for %.0f k-blocks (%.0f "
+                     "cyc/kb), start %.0f | mma wait-full %.0f wait-tempty %.0f | producer "
+                     "wait-empty %.0f | epi(thread) wait-tfull %.0f\n",
+                     acc[5] * 2, acc[6] * 2, acc[6] > 0 ? acc[5] / acc[6] : 0.0, acc[7] * 2,
+                     acc[1] * 2, acc[2] * 2, acc[0], acc[3] / 128);
+        std::fprintf(stderr, "[fqg gemm pair] SM clock during the MMA loop: %.0f MHz\n",
+                     acc[4] > 0 ? acc[5] / acc[4] * 1e3 : 0.0);
+        unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
+        for (int c = 0; c < nc; ++c) {
+            s0 = std::min<unsigned long long>(s0, h[c][0]);
+            s1 = std::max<unsigned long long>(s1, h[c][0]);
+            e0 = std::min<unsigned long long>(e0, h[c][3]);
+            e1 = std::max<unsigned long long>(e1, h[c][3]);
+        }
+        std::fprintf(stderr,
+                     "[fqg gemm pair] CTA start spread %.1f us, end spread %.1f..%.1f us after "
+                     "first start; per-leader mma loop %.1f us avg\n",
+                     (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, (e1 - s0) * 1e-3, acc[4] * 2e-3);
+        std::fprintf(stderr, "[fqg gemm pair] epilogue per tile (warp 0 of 4): %.2f us\n",
+                     acc[2] > 0 ? acc[1] / acc[2] * 1e-3 : 0.0);
+    }
+}
+
+template <bool APK, bool BPK>
+void dispatch_pair(const GemmArgs& g, cudaStream_t s) {
+    constexpr int ST = 6;
+    switch (g.y_dtype) {
+        case FQG_I32: return launch_pair<ST, FQG_I32, APK, BPK>(g, s);
+        case FQG_F64: return launch_pair<ST, FQG_F64, APK, BPK>(g, s);
+        case FQG_F32: return launch_pair<ST, FQG_F32, APK, BPK>(g, s);
+        case FQG_F16: return launch_pair<ST, FQG_F16, APK, BPK>(g, s);
+        case FQG_BF16: return launch_pair<ST, FQG_BF16, APK, BPK>(g, s);
+        default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
+    }
+}
+
 template <int BN, bool APK, bool BPK>
 void dispatch_out(const GemmArgs& g, cudaStream_t s) {
     constexpr int ST = (APK || BPK) ? 4 : 4;
@@ -403,6 +762,14 @@ void dispatch_out(const GemmArgs& g, cudaStream_t s) {
         case FQG_BF16: return launch<BN, ST, FQG_BF16, APK, BPK>(g, s);
         default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
     }
+}
+
+void dispatch_pair_fmt(const GemmArgs& g, cudaStream_t s) {
+    const bool apk = g.a_fmt == FQG_I4, bpk = g.b_fmt == FQG_I4;
+    if (!apk && !bpk) return dispatch_pair<false, false>(g, s);
+    if (!apk && bpk) return dispatch_pair<false, true>(g, s);
+    if (apk && !bpk) return dispatch_pair<true, false>(g, s);
+    return dispatch_pair<true, true>(g, s);
 }
 
 template <int BN>
@@ -441,7 +808,17 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
     require(g.kp % 32 == 0, "gemm: K' must be a multiple of 32");
     // INT32 exactness: |acc| <= K' * 127 * 127 must stay below 2^31.
     require(g.kp * 127ll * 127ll < (1ll << 31), "gemm: K' too large for exact INT32 accumulation");
-    if (g.n <= 128)
+    // variant: 0 auto, 1 single-CTA 128 x BN tiles, 2 CTA-pair 256 x 256 tiles.
+    // FQG_GEMM_VARIANT overrides auto (tests exercise both kernels).
+    static const int env_variant = [] {
+        const char* e = std::getenv("FQG_GEMM_VARIANT");
+        return e ? std::atoi(e) : 0;
+    }();
+    int v = g.variant != 0 ? g.variant : env_variant;
+    if (v == 0) v = (g.m > BM && g.n > 128) ? 2 : 1;
+    if (v == 2)
+        dispatch_pair_fmt(g, stream);
+    else if (g.n <= 128)
         dispatch_fmt<128>(g, stream);
     else
         dispatch_fmt<256>(g, stream);

@@ -99,6 +99,14 @@ GatherMaps compile_maps(const Plan& px, const Plan& pw) {
     g.width_x = k + px.c_extend;
     g.wsrc.assign(g.kp - px.padded, -1);
     for (int64_t kq = px.padded; kq < g.kp; ++kq) g.wsrc[kq - px.padded] = static_cast<int32_t>(sw[kq]);
+    g.ecomp.assign(k, -1);
+    g.xsrc.assign(px.c_extend, 0);
+    for (int64_t j = 0; j < k; ++j) {
+        if (px.ext[j] == 0) continue;
+        g.ecomp[j] = static_cast<int32_t>(g.n_ext++);
+        for (int64_t q = 0; q < px.ext[j]; ++q)
+            g.xsrc[px.off[j] + q] = static_cast<int32_t>((g.ecomp[j] << 12) | (1 + q));
+    }
     for (int64_t j = 0; j < k; ++j) {
         require(px.ext[j] + 1 <= kMaxPieces, "plan_x: a channel has more than 4095 extensions");
         g.cap_x[j] = static_cast<int32_t>(px.ext[j] + 1);

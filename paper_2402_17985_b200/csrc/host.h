@@ -40,6 +40,10 @@ struct GatherMaps {
     std::vector<int32_t> amap, wmap, wcap;
     std::vector<int32_t> cap_x;     // [K] plan_x capacity E_x + 1
     std::vector<int32_t> off_x;     // [K] plan_x ext_offset
+    // Channels with extension slots get a compact index ecomp[j] (else -1);
+    // plan_x extension slot K + i holds piece p of channel j: xsrc[i] = ecomp[j] << 12 | p.
+    std::vector<int32_t> ecomp, xsrc;
+    int64_t n_ext = 0;
     std::vector<int32_t> capw_src;  // [K] plan_w capacity of source row j
     // Final columns [C1, K') are plan_w extension copies of flattened columns:
     // wsrc[k' - C1] = r, or -1 for plan_w alignment padding.
