@@ -107,12 +107,7 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
 
 
-def shard_bounds(n: int, world: int, rank: int, align: int = 32):
-    """Column shard [b0, b1) of rank: contiguous, multiples of `align` except the last."""
-    per = -(-n // world)
-    per = -(-per // align) * align
-    b0 = min(n, rank * per)
-    return b0, min(n, b0 + per)
+from paper_2402_17985_b200.shard import gather_columns, shard_bounds  # noqa: E402
 
 
 def cpu_reference_sample(k, n, bits, rows, threads, steps=1, warmup=0, recipe_layer=None):
@@ -219,8 +214,6 @@ def main():
     ldq = kp // 2 if a_fmt == fq.I4 else kp
     q = torch.empty((m, ldq), dtype=torch.int8, device=xt.device)
     y = torch.empty((m, b1 - b0), dtype=torch.float16, device=xt.device)
-    gathered = torch.empty((world, m, b1 - b0), dtype=torch.float16, device=xt.device) \
-        if world > 1 else None
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=xt.device)
     st = torch.cuda.current_stream()
 
@@ -234,7 +227,7 @@ def main():
 
     def gather():
         if world > 1:
-            dist.all_gather_into_tensor(gathered, y)
+            gather_columns(y, n)  # NCCL all-gather of the column shards -> [M, N]
 
     for _ in range(args.warmup):
         k1()

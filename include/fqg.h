@@ -150,6 +150,18 @@ int fqg_build_flatten_plan(const double* maxes, int64_t k, double t, int64_t blo
 /* fq::split_against_threshold (flatten.cpp:8-15). */
 void fqg_split_against_threshold(double abs_value, double t, int64_t* count, double* rem);
 
+/* The composite gather maps the layer compiles from plan_x / plan_w (host
+ * only): for every final column k' of the flattened operands,
+ *   amap[k'] = j << 12 | p_x : activation column k' is piece p_x of channel j
+ *             (divide_columns -> flatten_tensor -> repeat_columns),
+ *   wmap[k'] = j << 12 | p_w : weight row k' is piece p_w of smoothed row j
+ *             (scale_rows -> repeat_channels -> flatten_rows),
+ *   wcap[k'] = the plan_w capacity E_w + 1 of that row; -1 marks padding.
+ * Arrays sized by `capacity` >= K' (returned in *kp). */
+int fqg_gather_maps(const int64_t* ext_x, int64_t k, int64_t block_x, const int64_t* ext_w,
+                    int64_t block_w, int32_t* amap, int32_t* wmap, int32_t* wcap, int64_t* kp,
+                    int64_t capacity);
+
 /* Offline recipe builder for modes O1/O2 with the bit width pinned by the
  * caller (KL bit selection, select_bit_width, is out of scope): the same
  * stage order as fq::quantize_layer (pipeline.cpp:76-152). Channel maxima of

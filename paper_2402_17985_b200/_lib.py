@@ -112,6 +112,7 @@ SIGNATURES = {
                               C.POINTER(F64_), P, C.POINTER(I64), C.POINTER(F64_), P, I64,
                               C.POINTER(I64), C.POINTER(F64_)]),
     "fqg_collect_channel_maxes": (None, [P, I64, I64, P]),
+    "fqg_gather_maps": (INT, [P, I64, I64, P, I64, P, P, P, C.POINTER(I64), I64]),
     "fqg_synth_default": (None, [C.POINTER(SynthOpts)]),
     "fqg_synthetic_layer": (INT, [C.POINTER(SynthOpts), I64, P, P, P, I64]),
 }

@@ -312,6 +312,21 @@ int fqg_recipe_plan(const double* weight, int64_t k, int64_t n, const double* ac
     });
 }
 
+int fqg_gather_maps(const int64_t* ext_x, int64_t k, int64_t block_x, const int64_t* ext_w,
+                    int64_t block_w, int32_t* amap, int32_t* wmap, int32_t* wcap, int64_t* kp,
+                    int64_t capacity) {
+    return guard([&] {
+        const Plan px = plan_from_ext(1.0, ext_x, k, block_x);
+        const Plan pw = plan_from_ext(1.0, ext_w, px.padded, block_w);
+        const GatherMaps g = compile_maps(px, pw);
+        *kp = g.kp;
+        require(capacity >= g.kp, "gather_maps: output capacity smaller than K'");
+        std::copy(g.amap.begin(), g.amap.end(), amap);
+        std::copy(g.wmap.begin(), g.wmap.end(), wmap);
+        std::copy(g.wcap.begin(), g.wcap.end(), wcap);
+    });
+}
+
 void fqg_synth_default(fqg_synth_opts* o) {
     *o = {32, 8, 128, 128, 0.01, 20.0, 100.0, 0.5, 0.08, 5.0, 0.25, 42};
 }
