@@ -290,7 +290,7 @@ __device__ __forceinline__ uint4 pack_i4(uint4 lo, uint4 hi) {
 // vectors; columns [C1, K') are plan_w copies of flat columns wsrc[k' - C1],
 // gathered bytewise.
 template <typename XT, bool PACK4>
-__global__ void __launch_bounds__(256, 3)
+__global__ void __launch_bounds__(256, 4)
     k_flatten_quant(const XT* __restrict__ x, int64_t ldx, int m, int k, int rows, int vec_ok,
                     const double* __restrict__ s, const double* __restrict__ rs,
                     const float* __restrict__ rs32, const int32_t* __restrict__ cap,
@@ -320,53 +320,56 @@ __global__ void __launch_bounds__(256, 3)
     const bool vec = vec_ok != 0;
 
     // ---- phase 1 ----
+    // Tier 1 (every element, ~12 instructions): z = |x| * RN32(1/(s_j*s_x)) is
+    // |v|/s_x = u*Q within 2e-7 relative. If z < Q(1 - 4e-7) then u < 1 for
+    // sure: no full pieces, no saturation, slot j holds round(|v|/s_x) — taken
+    // when z is also clear of a rounding half-integer. Tier 2 (flagged
+    // elements only, per-thread bitmask loop): the general FP32-certified split
+    // with the exact FP64 fallback.
+    const float ras32 = static_cast<float>(sc.ras);
+    const float qlo = sc.q32 * (1.0f - 4e-7f);
     unsigned long long sat = 0;
     for (int j0 = threadIdx.x * 8; j0 < k; j0 += blockDim.x * 8) {
         const int nj = min(8, k - j0);
-        float rj[8];
+        float rj[8], cz[8];
         int cj[8];
-        bool any_ext = false;
+        unsigned extm = 0;  // channels of this chunk with extension slots
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
             const int j = min(j0 + e, k - 1);
             rj[e] = __ldg(rs32 + j);
+            cz[e] = __fmul_rn(rj[e], ras32);
             cj[e] = __ldg(cap + j);
-            any_ext |= (e < nj) && cj[e] > 1;
+            extm |= (e < nj && cj[e] > 1) ? (1u << e) : 0u;
         }
         for (int r = 0; r < nrows; ++r) {
             float xf[8];
             double xd[8];
             load8f<XT>(x + static_cast<int64_t>(row0 + r) * ldx + j0, vec, nj, xf, xd);
             int8_t* fr = flat + r * c1;
+            uint32_t* cr = codes + r * n_ext;
             uint32_t w0 = 0u, w1 = 0u;
+            unsigned slow = 0;
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const Fast f = fast_elem(xf[e], rj[e], cj[e], sc);
-                const bool zero = xd[e] == 0.0;
-                uint64_t res;  // cnt | qrem << 16 | neg << 32 | sat << 33
-                if (zero || f.ok || e >= nj) {
-                    res = zero ? 0ull
-                               : (static_cast<uint64_t>(f.cnt) |
-                                  (static_cast<uint64_t>(f.qrem & 0xFFFF) << 16) |
-                                  (static_cast<uint64_t>(f.neg) << 32) |
-                                  (static_cast<uint64_t>(f.sat) << 33));
-                } else {  // rare: exact FP64 path
-                    res = slow_elem(xd[e], s + j0 + e, rs + j0 + e, cj[e], sc);
-                }
-                const int ce = static_cast<int>(res & 0xFFFF);
-                const int qe = static_cast<int>(static_cast<int16_t>(res >> 16));
-                const int full = (res >> 32) & 1 ? -sc.qT : sc.qT;
-                sat += (e < nj) ? ((res >> 33) & 1) : 0;
-                // slot j = piece 0: a full piece if cnt >= 1, else the remainder.
-                const uint32_t q0 = static_cast<uint32_t>((ce >= 1 ? full : qe) & 0xFF);
+                const float z = __fmul_rn(fabsf(xf[e]), cz[e]);
+                const float tz = __fadd_rn(z, 0.5f);
+                const float qf = floorf(tz);
+                const float d = __fsub_rn(tz, qf);
+                const float eps = __fadd_rn(__fmul_rn(z, 4e-7f), 1e-6f);
+                const bool ok = z < qlo && d > eps && d < 1.0f - eps;
+                const bool neg = xf[e] < 0.0f;
+                const int qi = static_cast<int>(qf);
+                const int qs = neg ? -qi : qi;
+                const uint32_t byte = ok ? static_cast<uint32_t>(qs & 0xFF) : 0u;
                 if (e < 4)
-                    w0 |= q0 << (8 * e);
+                    w0 |= byte << (8 * e);
                 else
-                    w1 |= q0 << (8 * (e - 4));
-                if (any_ext && e < nj && cj[e] > 1)  // channel with extension slots
-                    codes[r * n_ext + __ldg(ecomp + j0 + e)] =
-                        static_cast<uint32_t>(ce) | (static_cast<uint32_t>(qe & 0xFF) << 16) |
-                        (static_cast<uint32_t>((res >> 32) & 1) << 24);
+                    w1 |= byte << (8 * (e - 4));
+                slow |= (!ok && e < nj) ? (1u << e) : 0u;
+                if (ok && (extm & (1u << e)))  // remainder-only code: cnt 0, q = qs
+                    cr[__ldg(ecomp + j0 + e)] = static_cast<uint32_t>(qs & 0xFF) << 16 |
+                                                static_cast<uint32_t>(neg) << 24;
             }
             if (nj == 8) {
                 *reinterpret_cast<uint2*>(fr + j0) = make_uint2(w0, w1);
@@ -374,6 +377,33 @@ __global__ void __launch_bounds__(256, 3)
 #pragma unroll
                 for (int e = 0; e < 8; ++e)
                     if (e < nj) fr[j0 + e] = static_cast<int8_t>((e < 4 ? w0 : w1) >> (8 * (e & 3)));
+            }
+            while (slow) {  // tier 2
+                const int e = __ffs(slow) - 1;
+                slow &= slow - 1;
+                const int j = j0 + e;
+                const int cap_e = __ldg(cap + j);
+                const double xde = to_f64(x[static_cast<int64_t>(row0 + r) * ldx + j]);
+                const float xfe = static_cast<float>(xde);
+                const Fast f = fast_elem(xfe, __ldg(rs32 + j), cap_e, sc);
+                uint64_t res;  // cnt | qrem << 16 | neg << 32 | sat << 33
+                if (f.ok) {
+                    res = static_cast<uint64_t>(f.cnt) |
+                          (static_cast<uint64_t>(f.qrem & 0xFFFF) << 16) |
+                          (static_cast<uint64_t>(f.neg) << 32) | (static_cast<uint64_t>(f.sat) << 33);
+                } else {  // exact FP64 path
+                    res = slow_elem(xde, s + j, rs + j, cap_e, sc);
+                }
+                const int ce = static_cast<int>(res & 0xFFFF);
+                const int qe = static_cast<int>(static_cast<int16_t>(res >> 16));
+                const bool ng = (res >> 32) & 1;
+                sat += (res >> 33) & 1;
+                // slot j = piece 0: a full piece if cnt >= 1, else the remainder.
+                fr[j] = static_cast<int8_t>(ce >= 1 ? (ng ? -sc.qT : sc.qT) : qe);
+                if (cap_e > 1)
+                    cr[__ldg(ecomp + j)] = static_cast<uint32_t>(ce) |
+                                           (static_cast<uint32_t>(qe & 0xFF) << 16) |
+                                           (static_cast<uint32_t>(ng) << 24);
             }
         }
     }

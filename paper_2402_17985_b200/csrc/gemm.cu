@@ -54,7 +54,7 @@ struct Layout {
     static constexpr int bar_off = unp_off + USTAGES * unp_stage;
     static constexpr int n_bars = 2 * STAGES + 2 * USTAGES + 4;
     static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;  // + alignment slack
-    static constexpr int unpack_warps = packed ? 4 : 0;
+    static constexpr int unpack_warps = packed ? 8 : 0;
     static constexpr int threads = 256 + 32 * unpack_warps;
     // Arrivals that free a raw stage: the MMA commit if it reads an int8
     // operand straight from the raw stage, plus one per unpack warp.
@@ -80,6 +80,7 @@ __device__ __forceinline__ void unpack16(uint4 p, uint4& o0, uint4& o1) {
 // 128B-swizzle K-major layout: 16-byte chunk c of row r at r*128 + ((c ^ r%8) * 16).
 __device__ __forceinline__ void unpack_tile(const uint8_t* src, uint8_t* dst, int rows, int tid,
                                             int nthreads) {
+#pragma unroll 2
     for (int u = tid; u < rows * 4; u += nthreads) {
         const int r = u >> 2, pc = u & 3;
         const uint4 p = *reinterpret_cast<const uint4*>(src + r * 64 + pc * 16);
@@ -378,7 +379,7 @@ struct PairLayout {
     static constexpr int raw_stage = a_raw + b_raw;
     static constexpr int direct_bytes = (APK ? 0 : a_raw) + (BPK ? 0 : b_raw);
     static constexpr int packed_bytes = (APK ? a_raw : 0) + (BPK ? b_raw : 0);
-    static constexpr int USTAGES = packed ? 3 : 0;
+    static constexpr int USTAGES = packed ? 4 : 0;
     static constexpr int a_unp = APK ? BM * BK : 0;
     static constexpr int b_unp = BPK ? (BN / 2) * BK : 0;
     static constexpr int unp_stage = a_unp + b_unp;
@@ -386,7 +387,7 @@ struct PairLayout {
     static constexpr int bar_off = unp_off + USTAGES * unp_stage;
     static constexpr int n_bars = 3 * STAGES + 2 * USTAGES + 4;
     static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
-    static constexpr int unpack_warps = packed ? 4 : 0;
+    static constexpr int unpack_warps = packed ? 8 : 0;
     static constexpr int threads = 256 + 32 * unpack_warps;
     // Arrivals freeing a raw stage in each CTA: the leader's multicast MMA
     // commit when an operand is read straight from the raw stage, plus one per
@@ -815,7 +816,9 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
         return e ? std::atoi(e) : 0;
     }();
     int v = g.variant != 0 ? g.variant : env_variant;
-    if (v == 0) v = (g.m > BM && g.n > 128) ? 2 : 1;
+    // Measured (tools/gemm_sweep.py): the pair kernel wins for int8 x int8; with a
+    // packed int4 operand the single-CTA kernel's unpack pipeline is faster.
+    if (v == 0) v = (g.m > BM && g.n > 128 && g.a_fmt == FQG_I8 && g.b_fmt == FQG_I8) ? 2 : 1;
     if (v == 2)
         dispatch_pair_fmt(g, stream);
     else if (g.n <= 128)

@@ -60,10 +60,31 @@ static int fast_elem(float xf, float rs32, float rt32, float q32, int cap, float
     return 1;
 }
 
+
+/* K1 tier 1 (flatten.cu phase 1): z = |x| * RN32(RN32(1/s) * RN32(1/s_x)); if
+ * z < Q32 (1 - 4e-7) and z is clear of a rounding half-integer then
+ * cnt = 0, q = round(z) (sign applied), no saturation; else 0 = "flagged". */
+static int tier1_elem(float xf, float rs32, float ras32, float q32, int* cnt, int* qrem,
+                      int* sat) {
+    const float cz = rs32 * ras32;
+    const float z = fabsf(xf) * cz;
+    const float tz = z + 0.5f;
+    const float qf = floorf(tz);
+    const float d = tz - qf;
+    const float eps = z * 4e-7f + 1e-6f;
+    const float qlo = q32 * (1.0f - 4e-7f);
+    if (!(z < qlo && d > eps && d < 1.0f - eps)) return 0;
+    const int qi = (int)qf;
+    *cnt = 0;
+    *qrem = qi; /* magnitude; the kernel applies the sign like ref_elem's caller */
+    *sat = 0;
+    return 1;
+}
+
 int main(int argc, char** argv) {
     long long iters = argc > 1 ? atoll(argv[1]) : 100000000ll;
     if (argc > 2) s_ ^= (uint64_t)atoll(argv[2]) * 0x9E3779B97F4A7C15ull;
-    long long bad = 0, fb = 0;
+    long long bad = 0, fb = 0, bad1 = 0, t1 = 0;
     for (long long it = 0; it < iters; ++it) {
         const double s = exp((u01() - 0.5) * 6.0);
         double x = bf16_round((u01() - 0.5) * 8.0 * exp((u01() - 0.2) * 5.0));
@@ -75,6 +96,18 @@ int main(int argc, char** argv) {
         if ((it & 31) == 0) x = bf16_round(t * s * (double)(rnd() % 8)); /* near-exact fits */
         int c0, q0, s0, c1, q1, s1;
         ref_elem(x, s, t, as, cap, qmax, &c0, &q0, &s0);
+        {
+            int c2, q2, s2;
+            if (tier1_elem((float)x, (float)(1.0 / s), (float)(1.0 / as), (float)(t / as), &c2,
+                           &q2, &s2)) {
+                ++t1;
+                if (c2 != c0 || q2 != q0 || s2 != s0) {
+                    if (bad1++ < 10)
+                        printf("tier1 x=%a s=%a t=%a ref=(%d,%d,%d) t1=(%d,%d,%d)\n", x, s, t, c0,
+                               q0, s0, c2, q2, s2);
+                }
+            }
+        }
         if (!fast_elem((float)x, (float)(1.0 / s), (float)(1.0 / t), (float)(t / as), cap,
                        (float)qmax, &c1, &q1, &s1)) {
             ++fb;
@@ -86,7 +119,8 @@ int main(int argc, char** argv) {
                        q0, s0, c1, q1, s1);
         }
     }
-    printf("iters=%lld mismatches=%lld fallback=%lld (%.2e)\n", iters, bad, fb,
-           (double)fb / (double)iters);
-    return bad ? 1 : 0;
+    printf("iters=%lld mismatches=%lld fallback=%lld (%.2e) | tier1 taken=%lld (%.3f) "
+           "mismatches=%lld\n", iters, bad, fb, (double)fb / (double)iters, t1,
+           (double)t1 / (double)iters, bad1);
+    return (bad || bad1) ? 1 : 0;
 }
