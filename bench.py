@@ -41,12 +41,19 @@ SPEC_INT8_TOPS = 4500.0
 
 
 def peaks():
+    """(HBM GB/s, bf16 TFLOP/s, source, INT8 MMA TOPS, source)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["hbm_gbs"]), float(p["bf16_tflops"]), "MEASURED_PEAKS.json"
+        hbm, bf16, src = float(p["hbm_gbs"]), float(p["bf16_tflops"]), "MEASURED_PEAKS.json"
     except Exception:
-        return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+        hbm, bf16, src = 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+    try:  # MEASURED_PEAKS.json has no INT8 figure: our tcgen05 kind::i8 microbenchmark
+        with open(os.path.join(ROOT, "profiles", "measured_int8_peak.json")) as f:
+            i8, i8src = float(json.load(f)["int8_mma_tops"]), "measured (tools/mma_peak.cu)"
+    except Exception:
+        i8, i8src = 2.0 * bf16, f"2 x bf16 ({src})"
+    return hbm, bf16, src, i8, i8src
 
 
 class Clocks:
@@ -282,8 +289,7 @@ def main():
 
     ops = 2.0 * m * n * kp  # whole layer (all ranks), reference bitops K' (pipeline.cpp:211)
     tops = ops / (t_step * 1e-3) / 1e12
-    hbm_gbs, bf16_tf, peak_src = peaks()
-    int8_peak = 2.0 * bf16_tf  # INT8 dense = 2x BF16 dense on sm_100
+    hbm_gbs, bf16_tf, peak_src, int8_peak, i8_src = peaks()
     gemm_ops_rank = 2.0 * m * (b1 - b0) * kp
     gemm_tops = gemm_ops_rank / (t_k4 * 1e-3) / 1e12
     k1_bytes = m * k * 2 + m * ldq + kp * 4 + k * 12
@@ -315,8 +321,9 @@ def main():
         "roofline": {"bound": "tensor", "achieved": gemm_tops, "peak": int8_peak,
                      "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
                      "kernel": "k_gemm_i8 (tcgen05.mma kind::i8)",
-                     "peak_basis": f"INT8 dense = 2 x measured bf16 burst ({peak_src}); "
-                                   f"vs spec 4.5 POPS: {gemm_tops / SPEC_INT8_TOPS:.3f}",
+                     "peak_basis": f"tcgen05 kind::i8 MMA peak, {i8_src}; frac vs spec 4.5 "
+                                   f"POPS: {gemm_tops / SPEC_INT8_TOPS:.3f}; vs 2 x bf16 "
+                                   f"measured ({peak_src}): {gemm_tops / (2 * bf16_tf):.3f}",
                      "effective_tops_on_K": 2.0 * m * (b1 - b0) * k / (t_k4 * 1e-3) / 1e12},
         "roofline_k1": {"bound": "hbm", "achieved": k1_gbs, "peak": hbm_gbs, "unit": "GB/s",
                         "frac": k1_gbs / hbm_gbs, "bytes_per_launch": k1_bytes},

@@ -279,30 +279,36 @@ __device__ __forceinline__ uint4 pack_i4(uint4 lo, uint4 hi) {
     return make_uint4(p(lo.x, hi.x), p(lo.y, hi.y), p(lo.z, hi.z), p(lo.w, hi.w));
 }
 
-// One CTA = `rows` consecutive token rows.
+// One CTA = `rows` consecutive token rows; a shared-memory copy of each row's
+// plan_x-flattened form flat[r][0..C1) (slot j, extension slots
+// K + off_j + p - 1, zero padding; flatten.cpp:76-102) is built, then written.
+// Phase 0: zero the extension/padding region [K, C1).
 // Phase 1: every source element (i, j) is split once (thread owns 8
-// consecutive channels; tables reused across the CTA's rows) and its
-// quantized pieces are written straight into a shared-memory copy of the
-// plan_x-flattened row (flat[r][0..C1): slot j, extension slots
-// K + off_j + p - 1, zero padding).
+//   consecutive channels; tables reused across the CTA's rows). Tier 1 (every
+//   element, ~20 instructions) handles |v| < T: no full piece, so slot j holds
+//   the remainder q and every extension slot stays 0. Tier 2 (flagged elements
+//   only) runs the general FP32-certified split with the exact FP64 fallback;
+//   an element with pieces writes its single extension slot itself (E = 1) or
+//   queues (row, channel, count, remainder) for a warp-parallel expansion.
+// Phase 1b: warps expand queued elements, one lane per extension slot.
 // Phase 2: columns [0, C1) of the final operand ARE the flattened row
-// (repeat_columns keeps column r at r, flatten.cpp:166), copied with 16-byte
-// vectors; columns [C1, K') are plan_w copies of flat columns wsrc[k' - C1],
-// gathered bytewise.
+//   (repeat_columns keeps column r at r, flatten.cpp:166) — 16-byte copies;
+//   columns [C1, K') are plan_w copies of flat columns wsrc[k' - C1], gathered.
 template <typename XT, bool PACK4>
 __global__ void __launch_bounds__(256, 4)
     k_flatten_quant(const XT* __restrict__ x, int64_t ldx, int m, int k, int rows, int vec_ok,
                     const double* __restrict__ s, const double* __restrict__ rs,
                     const float* __restrict__ rs32, const int32_t* __restrict__ cap,
-                    const int32_t* __restrict__ ecomp, const int32_t* __restrict__ xsrc,
-                    int n_ext, const int32_t* __restrict__ wsrc, int c1, int width, int kp,
+                    const int32_t* __restrict__ off, int qcap,
+                    const int32_t* __restrict__ wsrc, int c1, int kp,
                     double t, double rt, double* __restrict__ scale,
                     const unsigned long long* __restrict__ amax, double qmax,
                     uint8_t* __restrict__ q, int64_t ldq, unsigned long long* __restrict__ sat_out) {
-    extern __shared__ uint4 flat4[];  // [rows][c1] bytes, then [rows][n_ext] codes
+    extern __shared__ uint4 flat4[];  // [rows][c1] bytes, then the expansion queue
     int8_t* flat = reinterpret_cast<int8_t*>(flat4);
-    uint32_t* codes = reinterpret_cast<uint32_t*>(flat + rows * c1);
+    uint2* queue = reinterpret_cast<uint2*>(flat + rows * c1);  // {code, r << 20 | j}
     __shared__ unsigned long long red[8];
+    __shared__ int qlen;
     const int row0 = blockIdx.x * rows;
     const int nrows = min(rows, m - row0);
     const double as = act_scale_of(scale, amax, qmax);
@@ -319,35 +325,36 @@ __global__ void __launch_bounds__(256, 4)
     sc.qT = quant(t, as, sc.ras, qmax);
     const bool vec = vec_ok != 0;
 
+    // ---- phase 0 ----
+    if (threadIdx.x == 0) qlen = 0;
+    {
+        const int k4 = (k + 3) & ~3;  // c1 is a multiple of 32: words from k4, bytes before
+        for (int r = 0; r < nrows; ++r) {
+            if (threadIdx.x < k4 - k) flat[r * c1 + k + threadIdx.x] = 0;
+            uint32_t* z = reinterpret_cast<uint32_t*>(flat + r * c1 + k4);
+            for (int i = threadIdx.x; i < (c1 - k4) >> 2; i += blockDim.x) z[i] = 0u;
+        }
+    }
+    __syncthreads();
+
     // ---- phase 1 ----
-    // Tier 1 (every element, ~12 instructions): z = |x| * RN32(1/(s_j*s_x)) is
-    // |v|/s_x = u*Q within 2e-7 relative. If z < Q(1 - 4e-7) then u < 1 for
-    // sure: no full pieces, no saturation, slot j holds round(|v|/s_x) — taken
-    // when z is also clear of a rounding half-integer. Tier 2 (flagged
-    // elements only, per-thread bitmask loop): the general FP32-certified split
-    // with the exact FP64 fallback.
+    // Tier 1: z = |x| * RN32(RN32(1/s_j) * RN32(1/s_x)) equals |v|/s_x = u*Q to
+    // within 2.4e-7 relative. z < Q(1 - 4e-7) proves u < 1: no full pieces,
+    // no saturation, slot j holds round(|v|/s_x) — accepted when z is also
+    // clear of a rounding half-integer (tools/verify_fp32_split.c, tier 1).
     const float ras32 = static_cast<float>(sc.ras);
     const float qlo = sc.q32 * (1.0f - 4e-7f);
     unsigned long long sat = 0;
     for (int j0 = threadIdx.x * 8; j0 < k; j0 += blockDim.x * 8) {
         const int nj = min(8, k - j0);
-        float rj[8], cz[8];
-        int cj[8];
-        unsigned extm = 0;  // channels of this chunk with extension slots
+        float cz[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const int j = min(j0 + e, k - 1);
-            rj[e] = __ldg(rs32 + j);
-            cz[e] = __fmul_rn(rj[e], ras32);
-            cj[e] = __ldg(cap + j);
-            extm |= (e < nj && cj[e] > 1) ? (1u << e) : 0u;
-        }
+        for (int e = 0; e < 8; ++e) cz[e] = __fmul_rn(__ldg(rs32 + min(j0 + e, k - 1)), ras32);
         for (int r = 0; r < nrows; ++r) {
             float xf[8];
             double xd[8];
             load8f<XT>(x + static_cast<int64_t>(row0 + r) * ldx + j0, vec, nj, xf, xd);
             int8_t* fr = flat + r * c1;
-            uint32_t* cr = codes + r * n_ext;
             uint32_t w0 = 0u, w1 = 0u;
             unsigned slow = 0;
 #pragma unroll
@@ -355,21 +362,17 @@ __global__ void __launch_bounds__(256, 4)
                 const float z = __fmul_rn(fabsf(xf[e]), cz[e]);
                 const float tz = __fadd_rn(z, 0.5f);
                 const float qf = floorf(tz);
-                const float d = __fsub_rn(tz, qf);
-                const float eps = __fadd_rn(__fmul_rn(z, 4e-7f), 1e-6f);
-                const bool ok = z < qlo && d > eps && d < 1.0f - eps;
-                const bool neg = xf[e] < 0.0f;
+                const float dd = fabsf(__fsub_rn(__fsub_rn(tz, qf), 0.5f));  // |frac - 1/2|
+                const float lim = __fsub_rn(0.5f, __fadd_rn(__fmul_rn(z, 4e-7f), 1e-6f));
+                const bool ok = z < qlo && dd < lim;
                 const int qi = static_cast<int>(qf);
-                const int qs = neg ? -qi : qi;
-                const uint32_t byte = ok ? static_cast<uint32_t>(qs & 0xFF) : 0u;
+                const uint32_t byte =
+                    ok ? static_cast<uint32_t>((xf[e] < 0.0f ? -qi : qi) & 0xFF) : 0u;
                 if (e < 4)
                     w0 |= byte << (8 * e);
                 else
                     w1 |= byte << (8 * (e - 4));
                 slow |= (!ok && e < nj) ? (1u << e) : 0u;
-                if (ok && (extm & (1u << e)))  // remainder-only code: cnt 0, q = qs
-                    cr[__ldg(ecomp + j0 + e)] = static_cast<uint32_t>(qs & 0xFF) << 16 |
-                                                static_cast<uint32_t>(neg) << 24;
             }
             if (nj == 8) {
                 *reinterpret_cast<uint2*>(fr + j0) = make_uint2(w0, w1);
@@ -384,8 +387,7 @@ __global__ void __launch_bounds__(256, 4)
                 const int j = j0 + e;
                 const int cap_e = __ldg(cap + j);
                 const double xde = to_f64(x[static_cast<int64_t>(row0 + r) * ldx + j]);
-                const float xfe = static_cast<float>(xde);
-                const Fast f = fast_elem(xfe, __ldg(rs32 + j), cap_e, sc);
+                const Fast f = fast_elem(static_cast<float>(xde), __ldg(rs32 + j), cap_e, sc);
                 uint64_t res;  // cnt | qrem << 16 | neg << 32 | sat << 33
                 if (f.ok) {
                     res = static_cast<uint64_t>(f.cnt) |
@@ -397,33 +399,42 @@ __global__ void __launch_bounds__(256, 4)
                 const int ce = static_cast<int>(res & 0xFFFF);
                 const int qe = static_cast<int>(static_cast<int16_t>(res >> 16));
                 const bool ng = (res >> 32) & 1;
+                const int full = ng ? -sc.qT : sc.qT;
                 sat += (res >> 33) & 1;
                 // slot j = piece 0: a full piece if cnt >= 1, else the remainder.
-                fr[j] = static_cast<int8_t>(ce >= 1 ? (ng ? -sc.qT : sc.qT) : qe);
-                if (cap_e > 1)
-                    cr[__ldg(ecomp + j)] = static_cast<uint32_t>(ce) |
-                                           (static_cast<uint32_t>(qe & 0xFF) << 16) |
-                                           (static_cast<uint32_t>(ng) << 24);
+                fr[j] = static_cast<int8_t>(ce >= 1 ? full : qe);
+                if (cap_e > 1 && ce >= 1) {  // extension slots carry pieces 1 .. E
+                    const int ext0 = k + __ldg(off + j);
+                    if (cap_e == 2) {
+                        fr[ext0] = static_cast<int8_t>(1 < ce ? full : (1 == ce ? qe : 0));
+                    } else {
+                        const int slot = atomicAdd(&qlen, 1);
+                        if (slot < qcap)
+                            queue[slot] = make_uint2(static_cast<uint32_t>(ce) |
+                                                         (static_cast<uint32_t>(qe & 0xFF) << 16) |
+                                                         (static_cast<uint32_t>(ng) << 24),
+                                                     (static_cast<uint32_t>(r) << 20) |
+                                                         static_cast<uint32_t>(j));
+                    }
+                }
             }
         }
     }
     __syncthreads();
-    // ---- phase 1b: extension slots [K, width) (piece p of channel j at
-    // K + off_j + p - 1, flatten.cpp:86-88) in parallel, and the alignment
-    // padding [width, C1) (zeros, flatten.cpp:43) ----
-    for (int r = 0; r < nrows; ++r) {
-        int8_t* fr = flat + r * c1;
-        const uint32_t* cr = codes + r * n_ext;
-        for (int i = threadIdx.x; i < c1 - k; i += blockDim.x) {
-            int v = 0;
-            if (k + i < width) {
-                const int xs = __ldg(xsrc + i);
-                const uint32_t code = cr[xs >> 12];
-                const int p = xs & 0xFFF, cnt = static_cast<int>(code & 0xFFFFu);
-                const int full = (code >> 24) & 1 ? -sc.qT : sc.qT;
-                v = p < cnt ? full : (p == cnt ? static_cast<int>(static_cast<int8_t>(code >> 16)) : 0);
-            }
-            fr[k + i] = static_cast<int8_t>(v);
+    // ---- phase 1b: warp-parallel expansion of queued elements ----
+    {
+        const int n_q = min(qlen, qcap);
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (int i = warp; i < n_q; i += blockDim.x >> 5) {
+            const uint2 e = queue[i];
+            const int j = static_cast<int>(e.y & 0xFFFFF), r = static_cast<int>(e.y >> 20);
+            const int cnt = static_cast<int>(e.x & 0xFFFFu);
+            const int qe = static_cast<int>(static_cast<int8_t>(e.x >> 16));
+            const int full = (e.x >> 24) & 1 ? -sc.qT : sc.qT;
+            const int ext = __ldg(cap + j) - 1;
+            int8_t* dst = flat + r * c1 + k + __ldg(off + j) - 1;  // dst[p], p = 1 .. E
+            for (int p = 1 + lane; p <= ext; p += 32)
+                dst[p] = static_cast<int8_t>(p < cnt ? full : (p == cnt ? qe : 0));
         }
     }
     __syncthreads();
@@ -619,11 +630,12 @@ void launch_flatten_t(const FlattenArgs& a, cudaStream_t st) {
                                                 a.rs, a.cap, a.t, rt, a.amax);
         FQG_CUDA(cudaGetLastError());
     }
-    const int64_t row_bytes = a.c1 + 4 * a.n_ext;  // flattened row + extension-channel codes
+    // flattened row + room to queue every channel with >= 2 extension slots
+    const int64_t row_bytes = a.c1 + 8 * a.n_ext2;
     // Rows per CTA: several rows amortize the table/map loads; keep >= ~4 CTAs per SM.
     int rows = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, (48 * 1024) / row_bytes)));
     while (rows > 1 && (a.m + rows - 1) / rows < 4 * a.num_sms) rows >>= 1;
-    const int64_t smem = rows * row_bytes;
+    const int64_t smem = (rows * a.c1 + 15) / 16 * 16 + rows * 8 * a.n_ext2;
     require(smem <= 200 * 1024, "flatten: plan_x width too large for the shared-memory row");
     const int grid = static_cast<int>((a.m + rows - 1) / rows);
     const bool vec = (reinterpret_cast<uintptr_t>(a.x) % 16 == 0) &&
@@ -633,9 +645,8 @@ void launch_flatten_t(const FlattenArgs& a, cudaStream_t st) {
                                       static_cast<int>(smem)));
         kern<<<grid, 256, smem, st>>>(static_cast<const XT*>(a.x), a.ldx, static_cast<int>(a.m),
                                       static_cast<int>(a.k), rows, vec ? 1 : 0, a.s, a.rs, a.rs32,
-                                      a.cap, a.ecomp, a.xsrc, static_cast<int>(a.n_ext), a.wsrc,
-                                      static_cast<int>(a.c1), static_cast<int>(a.width),
-                                      static_cast<int>(a.kp), a.t, rt,
+                                      a.cap, a.off, static_cast<int>(rows * a.n_ext2), a.wsrc,
+                                      static_cast<int>(a.c1), static_cast<int>(a.kp), a.t, rt,
                                       a.scale, a.amax, a.qmax, a.q, a.ldq, a.sat);
     };
     if (a.pack4)

@@ -15,9 +15,8 @@ struct FlattenArgs {
     const double* rs;             // [k] RN(1 / s), for the exact FMA-corrected division
     const float* rs32;            // [k] RN32(1 / s), FP32 fast path
     const int32_t* cap;           // [k] plan_x capacity E_x + 1
-    const int32_t* ecomp;         // [k] compact index of a channel with extensions, else -1
-    const int32_t* xsrc;          // [width - k] extension slot -> (compact channel << 12 | piece)
-    int64_t n_ext;                // channels with extensions
+    const int32_t* off;           // [k] plan_x ext_offset: piece p >= 1 of j at k + off + p - 1
+    int64_t n_ext2;               // channels with >= 2 extension slots (queue sizing)
     const int32_t* wsrc;          // [kp - c1] flat column copied into final column c1 + i, or -1
     const int32_t* amap;          // [kp] (j << 12 | p) or -1 (K2 / reference map)
     int64_t c1, width;            // plan_x.padded_width, plan_x.width()

@@ -41,8 +41,8 @@ struct fqg_layer_s {
     int64_t ldb = 0;
     double t_x = 0, t_w = 0, act_scale = 0, w_scale = 0, qmax = 127;
     int64_t width_x = 0;
-    int64_t n_ext = 0;
-    fqg::DevBuf d_s, d_rs, d_rs32, d_cap, d_ecomp, d_xsrc, d_wsrc, d_amap, d_wq, d_scale;
+    int64_t n_ext2 = 0;  // channels with >= 2 plan_x extension slots
+    fqg::DevBuf d_s, d_rs, d_rs32, d_cap, d_off, d_wsrc, d_amap, d_wq, d_scale;
 };
 
 namespace fqg {
@@ -139,9 +139,9 @@ fqg_layer_s* create(const fqg_layer_desc& d) {
         upload(L->d_rs, rs);
         upload(L->d_rs32, rs32);
         upload(L->d_cap, g.cap_x);
-        upload(L->d_ecomp, g.ecomp);
-        upload(L->d_xsrc, g.xsrc);
-        L->n_ext = g.n_ext;
+        upload(L->d_off, g.off_x);
+        L->n_ext2 = 0;
+        for (int64_t j = 0; j < d.k; ++j) L->n_ext2 += d.ext_x[j] >= 2 ? 1 : 0;
         upload(L->d_wsrc, g.wsrc);
         upload(L->d_amap, g.amap);
         L->width_x = g.width_x;
@@ -224,9 +224,8 @@ void quantize_acts(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, 
     a.rs = L->d_rs.as<double>();
     a.rs32 = L->d_rs32.as<float>();
     a.cap = L->d_cap.as<int32_t>();
-    a.ecomp = L->d_ecomp.as<int32_t>();
-    a.xsrc = L->d_xsrc.as<int32_t>();
-    a.n_ext = L->n_ext;
+    a.off = L->d_off.as<int32_t>();
+    a.n_ext2 = L->n_ext2;
     a.wsrc = L->d_wsrc.as<int32_t>();
     a.amap = L->d_amap.as<int32_t>();
     a.c1 = L->c1;
