@@ -29,8 +29,24 @@ struct FlattenArgs {
     int64_t ldq;
     unsigned long long* sat;      // optional saturation accumulator
     int num_sms;
+    // 16-bit fast path (flatten16.cu): per-channel certificate for this dtype
+    // (k_tier1_tables), or nullptr to use the general kernel.
+    const float* cj = nullptr;
+    const uint16_t* pj = nullptr;
+    const int32_t* hot = nullptr;  // channels always taking the exact path (pj = 0xFFFF)
+    int64_t nhot = 0;
+    const int32_t* wsrc16 = nullptr;  // wsrc with padding (-1) mapped to column kp (a zero byte)
+    double act_scale = 0.0;          // static s_x (host copy)
+    int32_t* rowsum = nullptr;    // optional [m] sums of each final operand row
 };
 void flatten_quant(const FlattenArgs& a, cudaStream_t st);
+
+// flatten16.cu: certificate tables for bf16 (f16 = false) or f16 inputs, and
+// the TMA-staged K1 (returns false when the call is outside its contract:
+// dtype, dynamic scale, alignment, shared-memory size).
+void tier1_tables(const double* s, int64_t k, double act_scale, double t, double qmax, bool f16,
+                  float* cj, uint16_t* pj, cudaStream_t st);
+bool flatten16(const FlattenArgs& a, cudaStream_t st);
 
 void weight_absmax(const double* w, int64_t k, int64_t ncols, const double* s,
                    const int32_t* capw_src, double t_w, unsigned long long* amax,

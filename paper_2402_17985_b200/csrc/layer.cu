@@ -11,6 +11,7 @@
 // Per forward (stream-ordered allocations): q [M][ldq] int8 / packed int4.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -43,6 +44,9 @@ struct fqg_layer_s {
     int64_t width_x = 0;
     int64_t n_ext2 = 0;  // channels with >= 2 plan_x extension slots
     fqg::DevBuf d_s, d_rs, d_rs32, d_cap, d_off, d_wsrc, d_amap, d_wq, d_scale;
+    // K1 16-bit certificates (flatten16.cu), static scale only: [0] bf16, [1] f16
+    fqg::DevBuf d_cj[2], d_pj[2], d_hot, d_wsrc16;
+    int64_t nhot = 0;
 };
 
 namespace fqg {
@@ -143,6 +147,11 @@ fqg_layer_s* create(const fqg_layer_desc& d) {
         L->n_ext2 = 0;
         for (int64_t j = 0; j < d.k; ++j) L->n_ext2 += d.ext_x[j] >= 2 ? 1 : 0;
         upload(L->d_wsrc, g.wsrc);
+        {  // K1 16-bit path: plan_w copy sources with padding -> the zero byte at column K'
+            std::vector<int32_t> w16(g.wsrc);
+            for (auto& v : w16) v = v < 0 ? static_cast<int32_t>(L->kp) : v;
+            upload(L->d_wsrc16, w16);
+        }
         upload(L->d_amap, g.amap);
         L->width_x = g.width_x;
 
@@ -189,6 +198,38 @@ fqg_layer_s* create(const fqg_layer_desc& d) {
         const double sc[2] = {d.scale_mode == FQG_SCALE_STATIC ? d.act_scale : 0.0, L->w_scale};
         L->d_scale.alloc(sizeof(sc));
         FQG_CUDA(cudaMemcpy(L->d_scale.p, sc, sizeof(sc), cudaMemcpyHostToDevice));
+        if (d.scale_mode == FQG_SCALE_STATIC && d.k % 8 == 0) {
+            for (int f = 0; f < 2; ++f) {
+                L->d_cj[f].alloc(static_cast<size_t>(d.k) * sizeof(float));
+                L->d_pj[f].alloc(static_cast<size_t>(d.k) * sizeof(uint16_t));
+                tier1_tables(L->d_s.as<double>(), d.k, d.act_scale, d.t_x, L->qmax, f == 1,
+                             L->d_cj[f].as<float>(), L->d_pj[f].as<uint16_t>(), 0);
+            }
+            // Hot channels: a calibrated maximum >= kHotE * T_x means most of the
+            // channel's elements carry full pieces; K1 runs them through the exact
+            // split on every row instead of queueing them (certificate P_j = 0xFFFF
+            // keeps them off the queue).
+            constexpr int64_t kHotE = 4;
+            constexpr size_t kMaxHot = 128;  // flatten16.cu: 32 lanes x kHotRegs
+            std::vector<int32_t> hot;
+            for (int64_t j = 0; j < d.k; ++j)
+                if (d.ext_x[j] >= kHotE) hot.push_back(static_cast<int32_t>(j));
+            if (hot.size() > kMaxHot) {  // keep the channels with the most extension slots
+                std::stable_sort(hot.begin(), hot.end(),
+                                 [&](int32_t a, int32_t b) { return d.ext_x[a] > d.ext_x[b]; });
+                hot.resize(kMaxHot);
+                std::sort(hot.begin(), hot.end());
+            }
+            L->nhot = static_cast<int64_t>(hot.size());
+            upload(L->d_hot, hot);
+            std::vector<uint16_t> pj(static_cast<size_t>(d.k));
+            for (int f = 0; f < 2 && !hot.empty(); ++f) {
+                FQG_CUDA(cudaMemcpy(pj.data(), L->d_pj[f].p, pj.size() * 2, cudaMemcpyDeviceToHost));
+                for (int32_t j : hot) pj[j] = 0xFFFF;
+                FQG_CUDA(cudaMemcpy(L->d_pj[f].p, pj.data(), pj.size() * 2, cudaMemcpyHostToDevice));
+            }
+            FQG_CUDA(cudaDeviceSynchronize());
+        }
         return L;
     } catch (...) {
         delete L;
@@ -239,6 +280,19 @@ void quantize_acts(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, 
     a.ldq = ldq_of(L);
     a.sat = sat;
     a.num_sms = num_sms(L->device);
+    static const bool general_only = [] {
+        const char* e = std::getenv("FQG_K1_GENERAL");
+        return e != nullptr && std::atoi(e) != 0;
+    }();
+    const int f = x_dtype == FQG_BF16 ? 0 : (x_dtype == FQG_F16 ? 1 : -1);
+    if (f >= 0 && amax == nullptr && !general_only && L->d_cj[f].p != nullptr) {
+        a.cj = L->d_cj[f].as<float>();
+        a.pj = L->d_pj[f].as<uint16_t>();
+        a.hot = L->d_hot.as<int32_t>();
+        a.nhot = L->nhot;
+        a.wsrc16 = L->d_wsrc16.as<int32_t>();
+        a.act_scale = L->act_scale;
+    }
     flatten_quant(a, st);
 }
 
