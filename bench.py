@@ -221,16 +221,19 @@ def main():
     ldq = kp // 2 if a_fmt == fq.I4 else kp
     q = torch.empty((m, ldq), dtype=torch.int8, device=xt.device)
     y = torch.empty((m, b1 - b0), dtype=torch.float16, device=xt.device)
+    rowsum = torch.empty(m, dtype=torch.int32, device=xt.device)  # K1 -> K4 (biased int4 weights)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=xt.device)
     st = torch.cuda.current_stream()
 
     def k1():
-        fq.check(fq.lib().fqg_layer_quantize_acts(layer._h, xt.data_ptr(), fq.BF16, m,
-                                                  q.data_ptr(), None, st.cuda_stream))
+        fq.check(fq.lib().fqg_layer_quantize_acts_ex(layer._h, xt.data_ptr(), fq.BF16, m,
+                                                     q.data_ptr(), rowsum.data_ptr(), None,
+                                                     st.cuda_stream))
 
     def k4():
-        fq.check(fq.lib().fqg_layer_gemm(layer._h, q.data_ptr(), m, y.data_ptr(), fq.F16,
-                                         y.stride(0), None, fq.NONE, st.cuda_stream))
+        fq.check(fq.lib().fqg_layer_gemm_ex(layer._h, q.data_ptr(), rowsum.data_ptr(), m,
+                                            y.data_ptr(), fq.F16, y.stride(0), None, fq.NONE,
+                                            st.cuda_stream))
 
     def gather():
         if world > 1:

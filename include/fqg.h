@@ -136,6 +136,18 @@ int fqg_layer_quantize_acts(fqg_layer_t layer, const void* x_dev, int x_dtype, i
 int fqg_layer_gemm(fqg_layer_t layer, const void* q_dev, int64_t m, void* y_dev, int y_dtype,
                    int64_t ldy, const void* bias_dev, int bias_dtype, void* stream);
 
+/* Same two halves with the operand row sums passed between them (optional
+ * rowsum_dev [m] int32). Int4 weights are stored with biased nibbles
+ * (q + 8) and multiplied as unsigned; the GEMM epilogue subtracts 8 * rowsum
+ * per row. fqg_layer_quantize_acts_ex writes the sums as a by-product;
+ * fqg_layer_gemm (or _ex with NULL) recomputes them with an extra pass. */
+int fqg_layer_quantize_acts_ex(fqg_layer_t layer, const void* x_dev, int x_dtype, int64_t m,
+                               void* q_dev, int32_t* rowsum_dev, unsigned long long* saturation_dev,
+                               void* stream);
+int fqg_layer_gemm_ex(fqg_layer_t layer, const void* q_dev, const int32_t* rowsum_dev, int64_t m,
+                      void* y_dev, int y_dtype, int64_t ldy, const void* bias_dev, int bias_dtype,
+                      void* stream);
+
 /* Standalone integer GEMM (int_matmul_raw / int_matmul, quantize.cpp:166-198):
  * a_dev [m][lda] and b_dev [n][ldb] K-major int8 (or packed int4), y as in
  * fqg_layer_forward; scale_dev: device double[2] = {s_x, s_w}; the epilogue forms s_x*s_w once in FP64 (quantize.cpp:193). */

@@ -105,6 +105,8 @@ SIGNATURES = {
     "fqg_layer_run_host": (INT, [P, P, I64, P, C.POINTER(I64)]),
     "fqg_layer_quantize_acts": (INT, [P, P, INT, I64, P, P, P]),
     "fqg_layer_gemm": (INT, [P, P, I64, P, INT, I64, P, INT, P]),
+    "fqg_layer_quantize_acts_ex": (INT, [P, P, INT, I64, P, P, P, P]),
+    "fqg_layer_gemm_ex": (INT, [P, P, P, I64, P, INT, I64, P, INT, P]),
     "fqg_gemm": (INT, [P, INT, I64, P, INT, I64, I64, I64, I64, P, INT, I64, P, P, INT, P]),
     "fqg_build_flatten_plan": (INT, [P, I64, F64_, I64, P, P, C.POINTER(I64), C.POINTER(I64)]),
     "fqg_split_against_threshold": (None, [F64_, F64_, C.POINTER(I64), C.POINTER(F64_)]),

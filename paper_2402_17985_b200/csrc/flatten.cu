@@ -476,7 +476,8 @@ __global__ void __launch_bounds__(256)
             uint32_t b = 0;
 #pragma unroll
             for (int e = 0; e < 4; ++e)
-                b |= static_cast<uint32_t>((lo[e] & 0xF) | ((hi[e] & 0xF) << 4)) << (8 * e);
+                // biased nibbles q + 8 (FQG_I4_BIASED, the layer's weight storage)
+                b |= static_cast<uint32_t>(((lo[e] + 8) & 0xF) | (((hi[e] + 8) & 0xF) << 4)) << (8 * e);
             *reinterpret_cast<uint32_t*>(wq + nn * ldq + k0 / 2 + 16 * g + i) = b;
         } else {
             const int kk = tx * 4;
@@ -489,6 +490,33 @@ __global__ void __launch_bounds__(256)
             *reinterpret_cast<uint32_t*>(wq + nn * ldq + k0 + kk) = b;
         }
     }
+}
+
+// Sum of each operand row (int8, or signed nibbles of packed int4): the row
+// sums the biased-int4 GEMM epilogue needs when K1 took the general path.
+__global__ void __launch_bounds__(256)
+    k_rowsum(const uint8_t* __restrict__ q, int64_t ldq, int m, int nbytes, bool pack4,
+             int32_t* __restrict__ out) {
+    const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (row >= m) return;
+    const uint4* r = reinterpret_cast<const uint4*>(q + row * ldq);
+    int acc = 0;
+    for (int i = lane; i < (nbytes >> 4); i += 32) {
+        const uint4 v = r[i];
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            if (pack4) {  // sum of (nibble ^ 8) = sum of (q + 8), 8 nibbles per word
+                acc += static_cast<int>(__dp4a((w[e] & 0x0F0F0F0Fu) ^ 0x08080808u, 0x01010101u, 0u));
+                acc += static_cast<int>(__dp4a(((w[e] >> 4) & 0x0F0F0F0Fu) ^ 0x08080808u, 0x01010101u, 0u));
+                acc -= 64;
+            } else {
+                acc = __dp4a(static_cast<int>(w[e]), 0x01010101, acc);
+            }
+        }
+    }
+    acc = static_cast<int>(warp_sum(static_cast<unsigned long long>(static_cast<int64_t>(acc))));
+    if (lane == 0) out[row] = acc;
 }
 
 template <typename XT>
@@ -535,12 +563,22 @@ void flatten_quant(const FlattenArgs& a, cudaStream_t st) {
     require(a.m >= 1 && a.k >= 1, "flatten: empty input");
     if (flatten16(a, st)) return;
     switch (a.x_dtype) {
-        case FQG_F64: return launch_flatten_t<double>(a, st);
-        case FQG_F32: return launch_flatten_t<float>(a, st);
-        case FQG_F16: return launch_flatten_t<__half>(a, st);
-        case FQG_BF16: return launch_flatten_t<__nv_bfloat16>(a, st);
+        case FQG_F64: launch_flatten_t<double>(a, st); break;
+        case FQG_F32: launch_flatten_t<float>(a, st); break;
+        case FQG_F16: launch_flatten_t<__half>(a, st); break;
+        case FQG_BF16: launch_flatten_t<__nv_bfloat16>(a, st); break;
         default: throw Error(FQG_ERR_INVALID, "flatten: unsupported activation dtype");
     }
+    if (a.rowsum != nullptr) operand_rowsum(a.q, a.ldq, a.m, a.kp, a.pack4, a.rowsum, st);
+}
+
+void operand_rowsum(const uint8_t* q, int64_t ldq, int64_t m, int64_t kp, bool pack4,
+                    int32_t* out, cudaStream_t st) {
+    require(ldq % 16 == 0 && reinterpret_cast<uintptr_t>(q) % 16 == 0,
+            "rowsum: operand rows must be 16-byte aligned");
+    k_rowsum<<<static_cast<unsigned>((m + 7) / 8), 256, 0, st>>>(
+        q, ldq, static_cast<int>(m), static_cast<int>(pack4 ? kp / 2 : kp), pack4, out);
+    FQG_CUDA(cudaGetLastError());
 }
 
 void weight_absmax(const double* w, int64_t k, int64_t ncols, const double* s,

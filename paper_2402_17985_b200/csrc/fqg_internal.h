@@ -62,6 +62,10 @@ int guard(F&& f) {
     }
 }
 
+// Internal operand format: packed int4 with biased nibbles (q + 8), the layer's
+// weight storage (gemm.cu); not part of the public ABI.
+constexpr int FQG_I4_BIASED = 106;
+
 // ---- K4: tcgen05 kind::i8 GEMM -------------------------------------------
 // Y[M, N] = epilogue( A[M, K'] . B[N, K']^T ), A/B K-major int8 or packed int4.
 struct GemmArgs {
@@ -79,6 +83,7 @@ struct GemmArgs {
     const void* bias;     // device [N] or nullptr
     int bias_dtype;
     int variant = 0;      // 0 auto, 1 single-CTA kernel, 2 CTA-pair kernel
+    const int32_t* rowsum = nullptr;  // [M] sum of each A row (FQG_I4_BIASED weights)
 };
 void gemm_i8(const GemmArgs& g, cudaStream_t stream);
 

@@ -33,6 +33,11 @@ namespace fqg {
 namespace {
 
 constexpr int BM = 128;       // UMMA M (cta_group::1)
+// Operand formats inside the kernels: int8 bytes, signed packed int4 (FQG_I4),
+// or biased packed int4 (stored nibble = q + 8, the layer's weight format: it
+// unpacks with one AND per 4 values and is fed to the MMA as UNSIGNED int8;
+// the epilogue subtracts 8 * rowsum(A) per output row, exact in int32).
+constexpr int F8 = 0, FS4 = 1, FU4 = 2;
 constexpr int BK = 128;       // K bytes per stage = one 128B swizzle row
 constexpr int UK = 32;        // K per tcgen05.mma kind::i8
 
@@ -58,7 +63,10 @@ struct Layout {
     static constexpr int threads = 256 + 32 * unpack_warps;
     // Arrivals that free a raw stage: the MMA commit if it reads an int8
     // operand straight from the raw stage, plus one per unpack warp.
-    static constexpr int raw_release = (APK && BPK ? 0 : 1) + unpack_warps;
+    // Unpack warps form two teams that take alternate k-blocks (two stages in
+    // flight); a stage is read by one team.
+    static constexpr int team_warps = unpack_warps / 2;
+    static constexpr int raw_release = (APK && BPK ? 0 : 1) + team_warps;
 };
 
 // FQG_I4 layout: per group of 32 k, byte i (0..15) = q[i] & 15 | q[16 + i] << 4.
@@ -76,20 +84,47 @@ __device__ __forceinline__ void unpack16(uint4 p, uint4& o0, uint4& o1) {
                     sext4x4((p.z >> 4) & 0x0F0F0F0Fu), sext4x4((p.w >> 4) & 0x0F0F0F0Fu));
 }
 
+// Biased nibbles u = q + 8 in [0, 15] -> unsigned bytes: one AND (low) and
+// SHIFT + AND (high) per 4 values.
+__device__ __forceinline__ void unpack16_biased(uint4 p, uint4& o0, uint4& o1) {
+    o0 = make_uint4(p.x & 0x0F0F0F0Fu, p.y & 0x0F0F0F0Fu, p.z & 0x0F0F0F0Fu, p.w & 0x0F0F0F0Fu);
+    o1 = make_uint4((p.x >> 4) & 0x0F0F0F0Fu, (p.y >> 4) & 0x0F0F0F0Fu, (p.z >> 4) & 0x0F0F0F0Fu,
+                    (p.w >> 4) & 0x0F0F0F0Fu);
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+
 // Expand `rows` x 64 packed bytes (plain rows) into rows x 128 int8 in the
 // 128B-swizzle K-major layout: 16-byte chunk c of row r at r*128 + ((c ^ r%8) * 16).
+// Shared-window 32-bit addresses (ld/st.shared), so no generic-address math.
+template <int FMT>
 __device__ __forceinline__ void unpack_tile(const uint8_t* src, uint8_t* dst, int rows, int tid,
                                             int nthreads) {
-#pragma unroll 2
+    const uint32_t s0 = ptx::smem_u32(src), d0 = ptx::smem_u32(dst);
+#pragma unroll 4
     for (int u = tid; u < rows * 4; u += nthreads) {
         const int r = u >> 2, pc = u & 3;
-        const uint4 p = *reinterpret_cast<const uint4*>(src + r * 64 + pc * 16);
+        const uint4 p = lds128(s0 + static_cast<uint32_t>(u) * 16);  // == r * 64 + pc * 16
         uint4 o0, o1;
-        unpack16(p, o0, o1);
-        uint8_t* row = dst + r * 128;
-        const int c0 = 2 * pc, c1 = 2 * pc + 1, sw = r & 7;
-        *reinterpret_cast<uint4*>(row + ((c0 ^ sw) << 4)) = o0;
-        *reinterpret_cast<uint4*>(row + ((c1 ^ sw) << 4)) = o1;
+        if constexpr (FMT == FU4)
+            unpack16_biased(p, o0, o1);
+        else
+            unpack16(p, o0, o1);
+        const uint32_t row = d0 + static_cast<uint32_t>(r) * 128;
+        const int sw = r & 7;
+        sts128(row + (((2 * pc) ^ sw) << 4), o0);
+        sts128(row + (((2 * pc + 1) ^ sw) << 4), o1);
     }
 }
 
@@ -120,9 +155,13 @@ __device__ __forceinline__ void store_one(void* y, int64_t idx, int32_t acc, dou
 
 // 32 consecutive columns of one row, from 32 accumulator registers.
 template <int OUT>
-__device__ __forceinline__ void store_row_chunk(void* y, int64_t base, const uint32_t (&r)[32],
+__device__ __forceinline__ void store_row_chunk(void* y, int64_t base, uint32_t (&r)[32],
                                                 double s, const void* bias, int bias_dt, int col0,
-                                                int ncols, bool vec) {
+                                                int ncols, bool vec, int32_t corr) {
+    if (corr != 0) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) r[c] = static_cast<uint32_t>(static_cast<int32_t>(r[c]) - corr);
+    }
     if (vec && ncols == 32) {
         if constexpr (OUT == FQG_I32) {
             int4* p = reinterpret_cast<int4*>(static_cast<int32_t*>(y) + base);
@@ -167,12 +206,13 @@ __device__ __forceinline__ void store_row_chunk(void* y, int64_t base, const uin
     }
 }
 
-template <int BN, int STAGES, int OUT, bool APK, bool BPK>
-__global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
+template <int BN, int STAGES, int OUT, int AF, int BF>
+__global__ void __launch_bounds__(Layout<BN, STAGES, AF != F8, BF != F8>::threads, 1)
     k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
               const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
-              int vec_ok) {
+              int vec_ok, const int32_t* __restrict__ rowsum) {
+    constexpr bool APK = AF != F8, BPK = BF != F8;
     using L = Layout<BN, STAGES, APK, BPK>;
     constexpr int U = L::USTAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -199,7 +239,7 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
             ptx::mbar_init(&empty[s], L::raw_release);
         }
         for (int u = 0; u < U; ++u) {
-            ptx::mbar_init(&ufull[u], L::unpack_warps);
+            ptx::mbar_init(&ufull[u], L::team_warps);
             ptx::mbar_init(&uempty[u], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -241,7 +281,7 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
-        constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+        constexpr uint32_t idesc = ptx::idesc_i8(BM, BN, BF == FU4);
         int stage = 0, us = 0;
         uint32_t phase = 0, uphase = 0;
         int it = 0;
@@ -293,6 +333,7 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             const int row = m_blk * BM + ew * 32 + lane;
+            const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
@@ -303,7 +344,7 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
                 if (row < m && col0 < n) {
                     const int ncols = min(32, n - col0);
                     store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
-                                         bias_dt, col0, ncols, vec_ok != 0);
+                                         bias_dt, col0, ncols, vec_ok != 0, corr);
                 }
             }
             ptx::tc_fence_before();
@@ -312,17 +353,29 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
         }
     } else if (L::packed && warp >= 8) {
         // ---------------- int4 -> int8 unpack warps ----------------
-        const int utid = threadIdx.x - 256, nut = 32 * L::unpack_warps;
-        int stage = 0, us = 0;
+        const int team = (warp - 8) / L::team_warps;
+        const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
+        int stage = 0, us = 0, step = 0;
         uint32_t phase = 0, uphase = 0;
         for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            for (int kb = 0; kb < num_kb; ++kb) {
+            for (int kb = 0; kb < num_kb; ++kb, ++step) {
+                if ((step & 1) != team) {
+                    if (++us == U) {
+                        us = 0;
+                        uphase ^= 1;
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    continue;
+                }
                 ptx::mbar_wait(&full[stage], phase);
                 ptx::mbar_wait(&uempty[us], uphase ^ 1);
                 const uint8_t* raw = smem + stage * L::raw_stage;
                 uint8_t* unp = smem + L::unp_off + us * L::unp_stage;
-                if constexpr (APK) unpack_tile(raw, unp, BM, utid, nut);
-                if constexpr (BPK) unpack_tile(raw + L::a_raw, unp + L::a_unp, BN, utid, nut);
+                if constexpr (APK) unpack_tile<AF>(raw, unp, BM, utid, nut);
+                if constexpr (BPK) unpack_tile<BF>(raw + L::a_raw, unp + L::a_unp, BN, utid, nut);
                 // generic-proxy smem writes -> visible to the tensor core (async proxy)
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
@@ -352,6 +405,13 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, APK, BPK>::threads, 1)
 // Developer instrumentation (FQG_GEMM_DEBUG=1): per-CTA cycles spent in each
 // role's barrier waits. Off by default (one predicated branch per wait).
 __device__ unsigned long long g_dbg[296][8];
+__device__ unsigned long long g_dbg2[296][8];  // pair packed path: see launch_pair
+#define FQG_TWAIT2(slot, ...)                                                  \
+    do {                                                                       \
+        const long long t0_ = dbg ? clock64() : 0;                             \
+        __VA_ARGS__;                                                           \
+        if (dbg) atomicAdd(&g_dbg2[blockIdx.x % 296][slot], clock64() - t0_);  \
+    } while (0)
 #define FQG_TWAIT(slot, ...)                                                   \
     do {                                                                       \
         const long long t0_ = dbg ? clock64() : 0;                             \
@@ -391,16 +451,18 @@ struct PairLayout {
     static constexpr int threads = 256 + 32 * unpack_warps;
     // Arrivals freeing a raw stage in each CTA: the leader's multicast MMA
     // commit when an operand is read straight from the raw stage, plus one per
-    // local unpack warp.
-    static constexpr int raw_release = (direct_bytes > 0 ? 1 : 0) + unpack_warps;
+    // local unpack warp that reads it.
+    static constexpr int team_warps = unpack_warps / 2;  // alternate k-blocks, as in Layout
+    static constexpr int raw_release = (direct_bytes > 0 ? 1 : 0) + (packed_bytes > 0 ? team_warps : 0);
 };
 
-template <int STAGES, int OUT, bool APK, bool BPK>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, APK, BPK>::threads, 1)
+template <int STAGES, int OUT, int AF, int BF>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, AF != F8, BF != F8>::threads, 1)
     k_gemm_i8_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
                    const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
-                   int vec_ok, int dbg) {
+                   int vec_ok, int dbg, const int32_t* __restrict__ rowsum) {
+    constexpr bool APK = AF != F8, BPK = BF != F8;
     using L = PairLayout<STAGES, APK, BPK>;
     const long long t_start = clock64();
     unsigned long long gstart = 0;
@@ -436,7 +498,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
             ptx::mbar_init(&empty[s], L::raw_release);
         }
         for (int u = 0; u < U; ++u) {
-            ptx::mbar_init(&ufull[u], 2 * L::unpack_warps);
+            ptx::mbar_init(&ufull[u], 2 * L::team_warps);  // one team's warps in both CTAs
             ptx::mbar_init(&uempty[u], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -489,7 +551,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         }
     } else if (warp == 1 && lane == 0 && leader) {
         // ---------------- MMA issuer (leader CTA) ----------------
-        constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN);
+        constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN, BF == FU4);
         int stage = 0, us = 0;
         uint32_t phase = 0, uphase = 0;
         int it = 0;
@@ -504,8 +566,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
             for (int kb = 0; kb < num_kb; ++kb) {
-                if constexpr (L::direct_bytes > 0) ptx::mbar_wait(&full_mma[stage], phase);
-                if constexpr (L::packed) ptx::mbar_wait(&ufull[us], uphase);
+                if constexpr (L::direct_bytes > 0) FQG_TWAIT2(1, ptx::mbar_wait(&full_mma[stage], phase));
+                if constexpr (L::packed) FQG_TWAIT2(0, ptx::mbar_wait(&ufull[us], uphase));
                 ptx::tc_fence_after();
                 const uint32_t raw = ptx::smem_u32(smem + stage * L::raw_stage);
                 const uint32_t unp = ptx::smem_u32(smem + L::unp_off + us * L::unp_stage);
@@ -555,6 +617,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
             unsigned long long ge0 = 0;
             if (dbg && lane == 0 && ew == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
             const int row = m_blk * 2 * BM + rank * BM + ew * 32 + lane;
+            const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
@@ -565,7 +628,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                 if (row < m && col0 < n) {
                     const int ncols = min(32, n - col0);
                     store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
-                                         bias_dt, col0, ncols, vec_ok != 0);
+                                         bias_dt, col0, ncols, vec_ok != 0, corr);
                 }
             }
             ptx::tc_fence_before();
@@ -580,17 +643,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         }
     } else if (L::packed && warp >= 8) {
         // ---------------- int4 -> int8 unpack warps (both CTAs) ----------------
-        const int utid = threadIdx.x - 256, nut = 32 * L::unpack_warps;
-        int stage = 0, us = 0;
+        const int team = (warp - 8) / L::team_warps;
+        const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
+        int stage = 0, us = 0, step = 0;
         uint32_t phase = 0, uphase = 0;
         for (int tile = cid; tile < num_tiles; tile += ncl) {
-            for (int kb = 0; kb < num_kb; ++kb) {
+            for (int kb = 0; kb < num_kb; ++kb, ++step) {
+                if ((step & 1) != team) {
+                    if (++us == U) {
+                        us = 0;
+                        uphase ^= 1;
+                    }
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    continue;
+                }
+                const bool d0 = dbg && utid == 0;
+                long long tw0 = d0 ? clock64() : 0;
                 ptx::mbar_wait(&full_unp[stage], phase);
+                long long tw1 = d0 ? clock64() : 0;
                 ptx::mbar_wait(&uempty[us], uphase ^ 1);
+                long long tw2 = d0 ? clock64() : 0;
                 const uint8_t* raw = smem + stage * L::raw_stage;
                 uint8_t* unp = smem + L::unp_off + us * L::unp_stage;
-                if constexpr (APK) unpack_tile(raw, unp, BM, utid, nut);
-                if constexpr (BPK) unpack_tile(raw + L::a_raw, unp + L::a_unp, BN / 2, utid, nut);
+                if constexpr (APK) unpack_tile<AF>(raw, unp, BM, utid, nut);
+                if constexpr (BPK) unpack_tile<BF>(raw + L::a_raw, unp + L::a_unp, BN / 2, utid, nut);
+                if (d0) {
+                    atomicAdd(&g_dbg2[blockIdx.x % 296][2], tw1 - tw0);
+                    atomicAdd(&g_dbg2[blockIdx.x % 296][3], tw2 - tw1);
+                    atomicAdd(&g_dbg2[blockIdx.x % 296][4], clock64() - tw2);
+                    atomicAdd(&g_dbg2[blockIdx.x % 296][5], 1ull);
+                }
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) {
@@ -638,8 +723,9 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-template <int BN, int STAGES, int OUT, bool APK, bool BPK>
+template <int BN, int STAGES, int OUT, int AF, int BF>
 void launch(const GemmArgs& g, cudaStream_t stream) {
+    constexpr bool APK = AF != F8, BPK = BF != F8;
     using L = Layout<BN, STAGES, APK, BPK>;
     static_assert(L::total <= 227 * 1024, "shared memory budget");
     CUtensorMap ta, tb;
@@ -650,7 +736,7 @@ void launch(const GemmArgs& g, cudaStream_t stream) {
     make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(BPK ? g.kp / 2 : g.kp),
                     static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.ldb), BPK ? BK / 2 : BK,
                     BN, BPK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
-    auto kern = k_gemm_i8<BN, STAGES, OUT, APK, BPK>;
+    auto kern = k_gemm_i8<BN, STAGES, OUT, AF, BF>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
@@ -665,12 +751,13 @@ void launch(const GemmArgs& g, cudaStream_t stream) {
     const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
     kern<<<grid, L::threads, L::total, stream>>>(ta, tb, g.y, g.ldy, static_cast<int>(g.m),
                                                  static_cast<int>(g.n), num_kb, g.scale, g.bias,
-                                                 g.bias_dtype, vec ? 1 : 0);
+                                                 g.bias_dtype, vec ? 1 : 0, g.rowsum);
     FQG_CUDA(cudaGetLastError());
 }
 
-template <int STAGES, int OUT, bool APK, bool BPK>
+template <int STAGES, int OUT, int AF, int BF>
 void launch_pair(const GemmArgs& g, cudaStream_t stream) {
+    constexpr bool APK = AF != F8, BPK = BF != F8;
     using L = PairLayout<STAGES, APK, BPK>;
     static_assert(L::total <= 227 * 1024, "shared memory budget");
     CUtensorMap ta, tb;
@@ -680,7 +767,7 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
     make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(BPK ? g.kp / 2 : g.kp),
                     static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.ldb), BPK ? BK / 2 : BK,
                     L::BN / 2, BPK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
-    auto kern = k_gemm_i8_pair<STAGES, OUT, APK, BPK>;
+    auto kern = k_gemm_i8_pair<STAGES, OUT, AF, BF>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
@@ -701,10 +788,11 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
     if (dbg) {
         static unsigned long long zeros[296][8] = {};
         FQG_CUDA(cudaMemcpyToSymbol(g_dbg, zeros, sizeof(zeros)));
+        FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
     }
     kern<<<2 * clusters, L::threads, L::total, stream>>>(
         ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb, g.scale, g.bias,
-        g.bias_dtype, vec ? 1 : 0, dbg);
+        g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum);
     FQG_CUDA(cudaGetLastError());
     if (dbg) {
         unsigned long long h[296][8];
@@ -736,50 +824,66 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
                      (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, (e1 - s0) * 1e-3, acc[4] * 2e-3);
         std::fprintf(stderr, "[fqg gemm pair] epilogue per tile (warp 0 of 4): %.2f us\n",
                      acc[2] > 0 ? acc[1] / acc[2] * 1e-3 : 0.0);
+        unsigned long long h2[296][8];
+        FQG_CUDA(cudaMemcpyFromSymbol(h2, g_dbg2, sizeof(h2)));
+        double a2[8] = {0};
+        for (int c = 0; c < nc; ++c)
+            for (int i = 0; i < 8; ++i) a2[i] += static_cast<double>(h2[c][i]) / nc;
+        std::fprintf(stderr,
+                     "[fqg gemm pair] per CTA: mma wait ufull %.0f, wait full_mma %.0f | unpack "
+                     "(thread 0): wait full_unp %.0f, wait uempty %.0f, work %.0f cyc over %.0f "
+                     "k-blocks\n",
+                     a2[0] * 2, a2[1] * 2, a2[2], a2[3], a2[4], a2[5]);
     }
 }
 
-template <bool APK, bool BPK>
+template <int AF, int BF>
 void dispatch_pair(const GemmArgs& g, cudaStream_t s) {
     constexpr int ST = 6;
     switch (g.y_dtype) {
-        case FQG_I32: return launch_pair<ST, FQG_I32, APK, BPK>(g, s);
-        case FQG_F64: return launch_pair<ST, FQG_F64, APK, BPK>(g, s);
-        case FQG_F32: return launch_pair<ST, FQG_F32, APK, BPK>(g, s);
-        case FQG_F16: return launch_pair<ST, FQG_F16, APK, BPK>(g, s);
-        case FQG_BF16: return launch_pair<ST, FQG_BF16, APK, BPK>(g, s);
+        case FQG_I32: return launch_pair<ST, FQG_I32, AF, BF>(g, s);
+        case FQG_F64: return launch_pair<ST, FQG_F64, AF, BF>(g, s);
+        case FQG_F32: return launch_pair<ST, FQG_F32, AF, BF>(g, s);
+        case FQG_F16: return launch_pair<ST, FQG_F16, AF, BF>(g, s);
+        case FQG_BF16: return launch_pair<ST, FQG_BF16, AF, BF>(g, s);
         default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
     }
 }
 
-template <int BN, bool APK, bool BPK>
+template <int BN, int AF, int BF>
 void dispatch_out(const GemmArgs& g, cudaStream_t s) {
-    constexpr int ST = (APK || BPK) ? 4 : 4;
+    constexpr int ST = 4;
     switch (g.y_dtype) {
-        case FQG_I32: return launch<BN, ST, FQG_I32, APK, BPK>(g, s);
-        case FQG_F64: return launch<BN, ST, FQG_F64, APK, BPK>(g, s);
-        case FQG_F32: return launch<BN, ST, FQG_F32, APK, BPK>(g, s);
-        case FQG_F16: return launch<BN, ST, FQG_F16, APK, BPK>(g, s);
-        case FQG_BF16: return launch<BN, ST, FQG_BF16, APK, BPK>(g, s);
+        case FQG_I32: return launch<BN, ST, FQG_I32, AF, BF>(g, s);
+        case FQG_F64: return launch<BN, ST, FQG_F64, AF, BF>(g, s);
+        case FQG_F32: return launch<BN, ST, FQG_F32, AF, BF>(g, s);
+        case FQG_F16: return launch<BN, ST, FQG_F16, AF, BF>(g, s);
+        case FQG_BF16: return launch<BN, ST, FQG_BF16, AF, BF>(g, s);
         default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
     }
 }
+
+int kfmt(int f) { return f == FQG_I8 ? F8 : (f == FQG_I4 ? FS4 : FU4); }
 
 void dispatch_pair_fmt(const GemmArgs& g, cudaStream_t s) {
-    const bool apk = g.a_fmt == FQG_I4, bpk = g.b_fmt == FQG_I4;
-    if (!apk && !bpk) return dispatch_pair<false, false>(g, s);
-    if (!apk && bpk) return dispatch_pair<false, true>(g, s);
-    if (apk && !bpk) return dispatch_pair<true, false>(g, s);
-    return dispatch_pair<true, true>(g, s);
+    const int af = kfmt(g.a_fmt), bf = kfmt(g.b_fmt);
+    if (af == F8 && bf == F8) return dispatch_pair<F8, F8>(g, s);
+    if (af == F8 && bf == FS4) return dispatch_pair<F8, FS4>(g, s);
+    if (af == F8 && bf == FU4) return dispatch_pair<F8, FU4>(g, s);
+    if (af == FS4 && bf == F8) return dispatch_pair<FS4, F8>(g, s);
+    if (af == FS4 && bf == FS4) return dispatch_pair<FS4, FS4>(g, s);
+    return dispatch_pair<FS4, FU4>(g, s);
 }
 
 template <int BN>
 void dispatch_fmt(const GemmArgs& g, cudaStream_t s) {
-    const bool apk = g.a_fmt == FQG_I4, bpk = g.b_fmt == FQG_I4;
-    if (!apk && !bpk) return dispatch_out<BN, false, false>(g, s);
-    if (!apk && bpk) return dispatch_out<BN, false, true>(g, s);
-    if (apk && !bpk) return dispatch_out<BN, true, false>(g, s);
-    return dispatch_out<BN, true, true>(g, s);
+    const int af = kfmt(g.a_fmt), bf = kfmt(g.b_fmt);
+    if (af == F8 && bf == F8) return dispatch_out<BN, F8, F8>(g, s);
+    if (af == F8 && bf == FS4) return dispatch_out<BN, F8, FS4>(g, s);
+    if (af == F8 && bf == FU4) return dispatch_out<BN, F8, FU4>(g, s);
+    if (af == FS4 && bf == F8) return dispatch_out<BN, FS4, F8>(g, s);
+    if (af == FS4 && bf == FS4) return dispatch_out<BN, FS4, FS4>(g, s);
+    return dispatch_out<BN, FS4, FU4>(g, s);
 }
 
 }  // namespace
@@ -805,7 +909,10 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
     require(g.m >= 1 && g.n >= 1 && g.kp >= 1, "gemm: empty shape");
     require(g.m < (1ll << 31) && g.n < (1ll << 31), "gemm: shape too large");
     require(g.a_fmt == FQG_I8 || g.a_fmt == FQG_I4, "gemm: operand A must be I8 or I4");
-    require(g.b_fmt == FQG_I8 || g.b_fmt == FQG_I4, "gemm: operand B must be I8 or I4");
+    require(g.b_fmt == FQG_I8 || g.b_fmt == FQG_I4 || g.b_fmt == FQG_I4_BIASED,
+            "gemm: operand B must be I8 or I4");
+    require(g.b_fmt != FQG_I4_BIASED || g.rowsum != nullptr,
+            "gemm: biased int4 weights need the operand row sums");
     require(g.kp % 32 == 0, "gemm: K' must be a multiple of 32");
     // INT32 exactness: |acc| <= K' * 127 * 127 must stay below 2^31.
     require(g.kp * 127ll * 127ll < (1ll << 31), "gemm: K' too large for exact INT32 accumulation");
@@ -818,7 +925,11 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
     int v = g.variant != 0 ? g.variant : env_variant;
     // Measured (tools/gemm_sweep.py): the pair kernel wins for int8 x int8; with a
     // packed int4 operand the single-CTA kernel's unpack pipeline is faster.
-    if (v == 0) v = (g.m > BM && g.n > 128 && g.a_fmt == FQG_I8 && g.b_fmt == FQG_I8) ? 2 : 1;
+    if (v == 0)
+        v = (g.m > BM && g.n > 128 && g.a_fmt == FQG_I8 &&
+             (g.b_fmt == FQG_I8 || g.b_fmt == FQG_I4_BIASED))
+                ? 2
+                : 1;
     if (v == 2)
         dispatch_pair_fmt(g, stream);
     else if (g.n <= 128)

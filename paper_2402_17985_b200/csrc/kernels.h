@@ -40,6 +40,9 @@ struct FlattenArgs {
     int32_t* rowsum = nullptr;    // optional [m] sums of each final operand row
 };
 void flatten_quant(const FlattenArgs& a, cudaStream_t st);
+// Row sums of a K1 operand [m][ldq] (int8, or signed packed int4).
+void operand_rowsum(const uint8_t* q, int64_t ldq, int64_t m, int64_t kp, bool pack4,
+                    int32_t* out, cudaStream_t st);
 
 // flatten16.cu: certificate tables for bf16 (f16 = false) or f16 inputs, and
 // the TMA-staged K1 (returns false when the call is outside its contract:

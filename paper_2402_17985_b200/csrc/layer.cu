@@ -81,7 +81,7 @@ std::vector<uint8_t> pack_weight_q(const int32_t* wq, int64_t kp, int64_t n_tota
             require(v >= -qmax && v <= qmax, "weight_q value outside [-qmax, qmax]");
             if (pack4) {
                 uint8_t& b = out[c * ldb + i4_byte(kq)];
-                b |= static_cast<uint8_t>((v & 0xF) << i4_shift(kq));
+                b |= static_cast<uint8_t>(((v + 8) & 0xF) << i4_shift(kq));  // biased nibble
             } else {
                 out[c * ldb + kq] = static_cast<uint8_t>(static_cast<int8_t>(v));
             }
@@ -251,10 +251,13 @@ struct CallScratch {
     }
 };
 
+bool biased_b(const fqg_layer_s* L) { return L->b_fmt == FQG_I4; }
+
 void quantize_acts(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, void* q,
                    double* scale, unsigned long long* amax, unsigned long long* sat,
-                   cudaStream_t st) {
+                   int32_t* rowsum, cudaStream_t st) {
     FlattenArgs a{};
+    a.rowsum = rowsum;
     a.x = x;
     a.x_dtype = x_dtype;
     a.ldx = L->k;
@@ -296,11 +299,28 @@ void quantize_acts(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, 
     flatten_quant(a, st);
 }
 
-void run_gemm(const fqg_layer_s* L, const void* q, int64_t m, void* y, int y_dtype, int64_t ldy,
-              const double* scale, const void* bias, int bias_dtype, cudaStream_t st) {
-    GemmArgs g{q, L->a_fmt, ldq_of(L), L->d_wq.p, L->b_fmt, L->ldb, m, L->n, L->kp,
-               y, y_dtype, ldy, scale, bias, bias ? bias_dtype : FQG_NONE};
-    gemm_i8(g, st);
+// Int4 weights are stored biased (nibble = q + 8, FQG_I4_BIASED): the GEMM
+// needs the operand row sums, from K1 or (when absent) from a rowsum pass.
+void run_gemm(const fqg_layer_s* L, const void* q, const int32_t* rowsum, int64_t m, void* y,
+              int y_dtype, int64_t ldy, const double* scale, const void* bias, int bias_dtype,
+              cudaStream_t st) {
+    int32_t* own = nullptr;
+    if (biased_b(L) && rowsum == nullptr) {
+        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&own), static_cast<size_t>(m) * 4, st));
+        operand_rowsum(static_cast<const uint8_t*>(q), ldq_of(L), m, L->kp, L->a_fmt == FQG_I4, own,
+                       st);
+        rowsum = own;
+    }
+    GemmArgs g{q, L->a_fmt, ldq_of(L), L->d_wq.p, biased_b(L) ? FQG_I4_BIASED : L->b_fmt, L->ldb,
+               m, L->n, L->kp, y, y_dtype, ldy, scale, bias, bias ? bias_dtype : FQG_NONE};
+    g.rowsum = rowsum;
+    try {
+        gemm_i8(g, st);
+    } catch (...) {
+        if (own) cudaFreeAsync(own, st);
+        throw;
+    }
+    if (own) FQG_CUDA(cudaFreeAsync(own, st));
 }
 
 void forward(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, void* y, int y_dtype,
@@ -311,7 +331,11 @@ void forward(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, void* 
     require(ldy >= L->n, "run_layer: ldy < n");
     CallScratch cs;
     cs.st = st;
-    FQG_CUDA(cudaMallocAsync(&cs.q, static_cast<size_t>(m * ldq_of(L)), st));
+    // q operand [m][ldq], then the row sums (16-byte aligned: ldq % 16 == 0)
+    const size_t qbytes = static_cast<size_t>(m * ldq_of(L));
+    FQG_CUDA(cudaMallocAsync(&cs.q, qbytes + (biased_b(L) ? static_cast<size_t>(m) * 4 : 0), st));
+    int32_t* rowsum =
+        biased_b(L) ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(cs.q) + qbytes) : nullptr;
     const double* scale = L->d_scale.as<double>();
     double* kscale = L->d_scale.as<double>();
     if (L->scale_mode == FQG_SCALE_DYNAMIC) {
@@ -321,8 +345,8 @@ void forward(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, void* 
         FQG_CUDA(cudaMemsetAsync(cs.amax, 0, 8, st));
         scale = kscale = cs.scale;
     }
-    quantize_acts(L, x, x_dtype, m, cs.q, kscale, cs.amax, sat, st);
-    run_gemm(L, cs.q, m, y, y_dtype, ldy, scale, bias, bias_dtype, st);
+    quantize_acts(L, x, x_dtype, m, cs.q, kscale, cs.amax, sat, rowsum, st);
+    run_gemm(L, cs.q, rowsum, m, y, y_dtype, ldy, scale, bias, bias_dtype, st);
 }
 
 }  // namespace
@@ -368,7 +392,7 @@ int fqg_layer_weight_q(fqg_layer_t L, int32_t* wq, double* w_scale) {
                     int v;
                     if (L->b_fmt == FQG_I4) {
                         const int nib = (packed[c * L->ldb + i4_byte(kq)] >> i4_shift(kq)) & 0xF;
-                        v = nib >= 8 ? nib - 16 : nib;
+                        v = nib - 8;  // biased storage
                     } else {
                         v = static_cast<int8_t>(packed[c * L->ldb + kq]);
                     }
@@ -390,27 +414,39 @@ int fqg_layer_forward(fqg_layer_t L, const void* x, int x_dtype, int64_t m, void
     });
 }
 
-int fqg_layer_quantize_acts(fqg_layer_t L, const void* x, int x_dtype, int64_t m, void* q,
-                            unsigned long long* saturation_dev, void* stream) {
+int fqg_layer_quantize_acts_ex(fqg_layer_t L, const void* x, int x_dtype, int64_t m, void* q,
+                               int32_t* rowsum_dev, unsigned long long* saturation_dev,
+                               void* stream) {
     return guard([&] {
         require(L != nullptr && x && q && m >= 1, "quantize_acts: bad argument");
         require(L->scale_mode == FQG_SCALE_STATIC,
                 "quantize_acts: the split entry points take the static scale");
         DeviceGuard dg(L->device);
         quantize_acts(L, x, x_dtype, m, q, L->d_scale.as<double>(), nullptr, saturation_dev,
-                      static_cast<cudaStream_t>(stream));
+                      rowsum_dev, static_cast<cudaStream_t>(stream));
+    });
+}
+
+int fqg_layer_quantize_acts(fqg_layer_t L, const void* x, int x_dtype, int64_t m, void* q,
+                            unsigned long long* saturation_dev, void* stream) {
+    return fqg_layer_quantize_acts_ex(L, x, x_dtype, m, q, nullptr, saturation_dev, stream);
+}
+
+int fqg_layer_gemm_ex(fqg_layer_t L, const void* q, const int32_t* rowsum_dev, int64_t m,
+                      void* y, int y_dtype, int64_t ldy, const void* bias, int bias_dtype,
+                      void* stream) {
+    return guard([&] {
+        require(L != nullptr && q && y && m >= 1, "layer_gemm: bad argument");
+        require(ldy >= L->n, "layer_gemm: ldy < n");
+        DeviceGuard dg(L->device);
+        run_gemm(L, q, rowsum_dev, m, y, y_dtype, ldy, L->d_scale.as<double>(), bias, bias_dtype,
+                 static_cast<cudaStream_t>(stream));
     });
 }
 
 int fqg_layer_gemm(fqg_layer_t L, const void* q, int64_t m, void* y, int y_dtype, int64_t ldy,
                    const void* bias, int bias_dtype, void* stream) {
-    return guard([&] {
-        require(L != nullptr && q && y && m >= 1, "layer_gemm: bad argument");
-        require(ldy >= L->n, "layer_gemm: ldy < n");
-        DeviceGuard dg(L->device);
-        run_gemm(L, q, m, y, y_dtype, ldy, L->d_scale.as<double>(), bias, bias_dtype,
-                 static_cast<cudaStream_t>(stream));
-    });
+    return fqg_layer_gemm_ex(L, q, nullptr, m, y, y_dtype, ldy, bias, bias_dtype, stream);
 }
 
 int fqg_layer_run_host(fqg_layer_t L, const double* x_host, int64_t m, double* y_host,

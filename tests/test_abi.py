@@ -19,6 +19,7 @@ def test_header_declares_the_boundary():
     names = header_functions()
     for required in ("fqg_layer_create", "fqg_layer_forward", "fqg_layer_run_host",
                      "fqg_layer_quantize_acts", "fqg_layer_gemm", "fqg_gemm",
+                     "fqg_layer_quantize_acts_ex", "fqg_layer_gemm_ex",
                      "fqg_layer_destroy", "fqg_last_error", "fqg_build_flatten_plan"):
         assert required in names
 

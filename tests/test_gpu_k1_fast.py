@@ -124,3 +124,35 @@ def test_forward_matches_oracle_bf16_odd_rows(port, fq):
     assert np.array_equal(acc.astype(np.int64), acc_ref)
     y = layer.forward(xt, out_dtype=torch.float64).cpu().numpy()
     assert np.array_equal(y, y_ref)
+
+
+@pytest.mark.parametrize("dtype,a_fmt_name", [("bf16", "I8"), ("bf16", "I4"), ("f32", "I8")])
+def test_rowsum_and_split_entry_points(port, fq, dtype, a_fmt_name):
+    """quantize_acts_ex row sums == sum of the operand row; gemm_ex with them
+    (biased int4 weights) == the oracle's INT32 accumulators."""
+    import torch
+
+    a_fmt = getattr(fq, a_fmt_name)
+    k, n, m = 1024, 192, 70
+    w, calib, x = fq.synthetic_layer(4, test_rows=m, in_channels=k, out_channels=n, rows=32,
+                                     samples=4)
+    L = port.quantize_layer(w, calib, 4)
+    x = bf16_round(x)
+    _, _, q_ref, acc_ref = port.run_layer(L, x, debug=True)
+    layer = fq.Layer(to_cfg(fq, L), a_format=a_fmt, b_format=fq.I4)
+    xt = torch.from_numpy(x).to(torch.bfloat16 if dtype == "bf16" else torch.float32).cuda()
+    cols = layer.kp // 2 if a_fmt == fq.I4 else layer.kp
+    q = torch.empty((m, cols), dtype=torch.int8, device="cuda")
+    rs = torch.empty(m, dtype=torch.int32, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    fq.check(fq.lib().fqg_layer_quantize_acts_ex(layer._h, xt.data_ptr(),
+                                                 fq._lib.BF16 if dtype == "bf16" else fq._lib.F32,
+                                                 m, q.data_ptr(), rs.data_ptr(), None, st))
+    torch.cuda.synchronize()
+    assert np.array_equal(rs.cpu().numpy().astype(np.int64), q_ref.sum(axis=1))
+    acc = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    fq.check(fq.lib().fqg_layer_gemm_ex(layer._h, q.data_ptr(), rs.data_ptr(), m, acc.data_ptr(),
+                                        fq._lib.I32, n, None, fq.NONE, st))
+    assert np.array_equal(acc.cpu().numpy().astype(np.int64), acc_ref)
+    acc2 = layer.gemm(q, out_dtype=torch.int32)  # row sums recomputed internally
+    assert np.array_equal(acc2.cpu().numpy().astype(np.int64), acc_ref)
