@@ -15,6 +15,15 @@ int num_sms(int device) {
     if (cache[device] == 0) {
         int v = 0;
         FQG_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device));
+        // Per-call scratch (K1 operand, GEMM stream-K workspace) comes from the
+        // device's default stream-ordered pool: keep freed blocks cached instead
+        // of returning them to the OS at every synchronisation (which makes the
+        // next cudaMallocAsync a real allocation, tens of microseconds).
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = ~0ull;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
         cache[device] = v;
     }
     return cache[device];

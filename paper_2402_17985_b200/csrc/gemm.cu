@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "fqg_internal.h"
@@ -461,7 +462,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
     k_gemm_i8_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
                    const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
-                   int vec_ok, int dbg, const int32_t* __restrict__ rowsum) {
+                   int vec_ok, int dbg, const int32_t* __restrict__ rowsum, int sk,
+                   int32_t* __restrict__ ws, int* __restrict__ ws_flag) {
     constexpr bool APK = AF != F8, BPK = BF != F8;
     using L = PairLayout<STAGES, APK, BPK>;
     const long long t_start = clock64();
@@ -488,6 +490,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
     const int num_n = (n + BN - 1) / BN;
     const int num_tiles = num_m * num_n;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    // Work of this cluster as segments (tile, kb0, kb1). Data-parallel: whole
+    // tiles round robin. Stream-K (sk): the tile x k-block units are cut into
+    // ncl equal contiguous ranges (each >= one tile, so a tile is split at
+    // most two ways): a range that starts inside a tile leaves its partial
+    // INT32 sums in ws[cid] (flag += 8 warps); the cluster that owns the tile's
+    // head adds ws[cid + 1] in its epilogue (integer sums: exact, order-free).
+    auto for_each_seg = [&](auto&& f) {
+        if (sk) {
+            const int64_t total = static_cast<int64_t>(num_tiles) * num_kb;
+            const int u0 = static_cast<int>(total * cid / ncl);
+            const int u1 = static_cast<int>(total * (cid + 1) / ncl);
+            for (int u = u0; u < u1;) {
+                const int tile = u / num_kb, kb0 = u % num_kb;
+                const int kb1 = min(num_kb, kb0 + (u1 - u));
+                f(tile, kb0, kb1);
+                u += kb1 - kb0;
+            }
+        } else {
+            for (int tile = cid; tile < num_tiles; tile += ncl) f(tile, 0, num_kb);
+        }
+    };
 
     if (threadIdx.x == 0) {
         ptx::tma_prefetch_desc(&tmA);
@@ -521,11 +544,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         const uint64_t keep = ptx::policy_evict_last();
         int stage = 0;
         uint32_t phase = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
+        for_each_seg([&](int tile, int kb0, int kb1) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const int a_row = m_blk * 2 * BM + rank * BM;
             const int b_row = n_blk * BN + rank * (BN / 2);
-            for (int kb = 0; kb < num_kb; ++kb) {
+            for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * L::raw_stage;
                 uint8_t* sb = sa + L::a_raw;
@@ -548,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                     phase ^= 1;
                 }
             }
-        }
+        });
     } else if (warp == 1 && lane == 0 && leader) {
         // ---------------- MMA issuer (leader CTA) ----------------
         constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN, BF == FU4);
@@ -559,13 +582,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         unsigned long long g0;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
         long long nkb_done = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+        for_each_seg([&](int, int kb0, int kb1) {
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             FQG_TWAIT(2, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < num_kb; ++kb) {
+            for (int kb = kb0; kb < kb1; ++kb) {
                 if constexpr (L::direct_bytes > 0) FQG_TWAIT2(1, ptx::mbar_wait(&full_mma[stage], phase));
                 if constexpr (L::packed) FQG_TWAIT2(0, ptx::mbar_wait(&ufull[us], uphase));
                 ptx::tc_fence_after();
@@ -577,7 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                 for (int k = 0; k < BK / UK; ++k) {
                     ptx::mma_i8_pair(d_tmem, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
                                      ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
-                                     (kb | k) != 0 ? 1u : 0u);
+                                     (kb != kb0 || k != 0) ? 1u : 0u);
                 }
                 if constexpr (L::direct_bytes > 0) ptx::mma_commit_pair(&empty[stage], 0x3);
                 if constexpr (L::packed) {
@@ -593,8 +616,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                 }
             }
             ptx::mma_commit_pair(&tfull[acc], 0x3);
-            nkb_done += num_kb;
-        }
+            nkb_done += kb1 - kb0;
+            ++it;
+        });
         if (dbg) {
             atomicAdd(&g_dbg[blockIdx.x % 296][5], clock64() - t_mma0);
             atomicAdd(&g_dbg[blockIdx.x % 296][6], static_cast<unsigned long long>(nkb_done));
@@ -608,22 +632,55 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         const int ew = warp - 4;
         const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
         int it = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+        for_each_seg([&](int tile, int kb0, int kb1) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
+            const bool tail = kb0 > 0;        // partial sums -> ws[cid]
+            const bool head = kb1 < num_kb;   // add ws[cid + 1] (its tail partial)
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             unsigned long long ge0 = 0;
             if (dbg && lane == 0 && ew == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
-            const int row = m_blk * 2 * BM + rank * BM + ew * 32 + lane;
+            const int rloc = rank * BM + ew * 32 + lane;  // row within the 256-row tile
+            const int row = m_blk * 2 * BM + rloc;
             const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+            if (head) {
+                if (lane == 0) {
+                    const long long tw0 = clock64();
+                    int v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ws_flag + cid + 1));
+                    } while (v < 8);
+                    if (dbg && ew == 0) {
+                        atomicAdd(&g_dbg2[blockIdx.x % 296][6], clock64() - tw0);
+                        atomicAdd(&g_dbg2[blockIdx.x % 296][7], clock64() - t_start);
+                    }
+                }
+                __syncwarp();
+            }
 #pragma unroll 1
             for (int c = 0; c < BN / 32; ++c) {
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
                 ptx::tmem_wait_ld();
+                if (tail) {
+                    int4* wp = reinterpret_cast<int4*>(ws + (static_cast<int64_t>(cid) * 256 + rloc) * 256 + c * 32);
+#pragma unroll
+                    for (int v = 0; v < 8; ++v)
+                        wp[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+                    continue;
+                }
+                if (head) {
+                    const int4* wp = reinterpret_cast<const int4*>(
+                        ws + (static_cast<int64_t>(cid + 1) * 256 + rloc) * 256 + c * 32);
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        const int4 pv = __ldcg(wp + v);
+                        r[4 * v] += pv.x, r[4 * v + 1] += pv.y, r[4 * v + 2] += pv.z, r[4 * v + 3] += pv.w;
+                    }
+                }
                 const int col0 = n_blk * BN + c * 32;
                 if (row < m && col0 < n) {
                     const int ncols = min(32, n - col0);
@@ -634,21 +691,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+            if (tail) {  // publish the partial: release at gpu scope, one arrival per warp
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicAdd(ws_flag + cid, 1);
+            }
             if (dbg && lane == 0 && ew == 0) {
                 unsigned long long ge1;
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge1));
                 atomicAdd(&g_dbg[blockIdx.x % 296][1], ge1 - ge0);
                 atomicAdd(&g_dbg[blockIdx.x % 296][2], 1ull);
             }
-        }
+            ++it;
+        });
     } else if (L::packed && warp >= 8) {
         // ---------------- int4 -> int8 unpack warps (both CTAs) ----------------
         const int team = (warp - 8) / L::team_warps;
         const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
         int stage = 0, us = 0, step = 0;
         uint32_t phase = 0, uphase = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
-            for (int kb = 0; kb < num_kb; ++kb, ++step) {
+        for_each_seg([&](int, int kb0, int kb1) {
+            for (int kb = kb0; kb < kb1; ++kb, ++step) {
                 if ((step & 1) != team) {
                     if (++us == U) {
                         us = 0;
@@ -691,7 +754,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                     phase ^= 1;
                 }
             }
-        }
+        });
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
@@ -705,6 +768,293 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gend));
         g_dbg[blockIdx.x % 296][0] = gstart;
         g_dbg[blockIdx.x % 296][3] = gend;
+    }
+}
+
+// ------------------------------------------------------------------------
+// Weights-in-TMEM kernel for biased int4 weights ("swap AB"): Y^T = W . X^T.
+// The 128 weight rows of a tile are the MMA's M side and live in TENSOR
+// memory: two teams of 4 unpack warps load the packed rows from L2 into
+// registers (64 bytes per lane per k-block), unpack the biased nibbles with
+// one AND per 4 values and tcgen05.st them into a 4-stage A ring in TMEM. The
+// activations (int8) are the N side: TMA -> 128B-swizzled SMEM ring. Shared
+// memory then only carries the activation tile (TMA write + MMA read), so the
+// int4 unpack no longer competes with the tensor core for SMEM bandwidth.
+// A is fed as UNSIGNED int8 (nibble = q + 8); the epilogue subtracts
+// 8 * rowsum(x_token) per output column (exact in int32).
+// TMEM: accumulators [0, 2 BN) (double-buffered), A stages [2 BN, 2 BN + 128).
+constexpr int kW4AStages = 4;
+template <int BN, int STAGES, int ESZ = 8>
+struct W4Layout {
+    static constexpr int b_stage = BN * BK;  // activation rows x 128 bytes
+    // epilogue transpose tiles: per warp 2 buffers of 32 tokens x 32 features
+    // (dense rows of 32 * ESZ bytes: the box a TMA tensor store writes)
+    static constexpr int epi_row = 32 * ESZ;
+    static constexpr int epi_buf = 32 * epi_row;
+    static constexpr int epi_off = STAGES * b_stage;
+    static constexpr int bar_off = epi_off + 4 * 2 * epi_buf;
+    static constexpr int n_bars = 2 * STAGES + 2 * kW4AStages + 4;
+    static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
+    static constexpr int threads = 512;
+    static constexpr uint32_t a_col0 = 2 * BN;
+    static_assert(2 * BN + 32 * kW4AStages <= 512, "TMEM budget");
+};
+
+template <int OUT>
+struct OutT;
+template <> struct OutT<FQG_I32> { using T = int32_t; };
+template <> struct OutT<FQG_F64> { using T = double; };
+template <> struct OutT<FQG_F32> { using T = float; };
+template <> struct OutT<FQG_F16> { using T = __half; };
+template <> struct OutT<FQG_BF16> { using T = __nv_bfloat16; };
+
+template <int OUT>
+__device__ __forceinline__ typename OutT<OUT>::T convert_out(int32_t acc, double s, double b) {
+    if constexpr (OUT == FQG_I32) {
+        return acc;
+    } else {
+        const double v = static_cast<double>(acc) * s + b;  // quantize.cpp:196 (+ bias)
+        if constexpr (OUT == FQG_F64) return v;
+        if constexpr (OUT == FQG_F32) return static_cast<float>(v);
+        if constexpr (OUT == FQG_F16) return __double2half(v);
+        if constexpr (OUT == FQG_BF16) return __double2bfloat16(v);
+    }
+}
+
+template <int BN, int STAGES, int OUT>
+__global__ void __launch_bounds__(512, 1)
+    k_gemm_w4t(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w,
+               int64_t ldb, int kbytes, void* __restrict__ y, int64_t ldy, int m, int n,
+               int num_kb, const double* __restrict__ scale, const void* __restrict__ bias,
+               int bias_dt, const int32_t* __restrict__ rowsum, int vec_ok, int dbg,
+               const __grid_constant__ CUtensorMap tmY, int tma_y) {
+    using OT = typename OutT<OUT>::T;
+    constexpr int ESZ = sizeof(OT);
+    using L = W4Layout<BN, STAGES, ESZ>;
+    constexpr int AS = kW4AStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);
+    uint64_t* empty = full + STAGES;
+    uint64_t* afull = empty + STAGES;
+    uint64_t* aempty = afull + AS;
+    uint64_t* tfull = aempty + AS;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int num_t = (m + BN - 1) / BN, num_f = (n + 127) / 128;
+    const int num_tiles = num_t * num_f;
+    if (threadIdx.x == 0) {
+        ptx::tma_prefetch_desc(&tmX);
+        for (int i = 0; i < STAGES; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < AS; ++i) {
+            ptx::mbar_init(&afull[i], 4);  // the 4 warps of the team that filled it
+            ptx::mbar_init(&aempty[i], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc(tmem_holder, 512);
+        ptx::tmem_relinquish();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer: activation tiles ----------------
+        const uint64_t keep = ptx::policy_evict_last();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            const int t_blk = tile % num_t;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                ptx::mbar_arrive_expect_tx(&full[stage], L::b_stage);
+                ptx::tma_load_2d_hint(smem + stage * L::b_stage, &tmX, &full[stage], kb * BK,
+                                      t_blk * BN, keep);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer: A (weights) from TMEM, B from SMEM ----------------
+        constexpr uint32_t idesc = ptx::idesc_i8(128, BN, /*b_unsigned=*/false, /*a_unsigned=*/true);
+        int stage = 0, as = 0, it = 0;
+        uint32_t phase = 0, aphase = 0;
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            const int acc = it & 1;
+            FQG_TWAIT2(0, ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1));
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                FQG_TWAIT2(1, ptx::mbar_wait(&full[stage], phase));
+                FQG_TWAIT2(2, ptx::mbar_wait(&afull[as], aphase));
+                ptx::tc_fence_after();
+                const uint32_t a_tmem = tmem_base + L::a_col0 + as * 32;
+                const uint32_t b_addr = ptx::smem_u32(smem + stage * L::b_stage);
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k)
+                    ptx::mma_i8_ts(d_tmem, a_tmem + k * (UK / 4),
+                                   ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
+                                   (kb | k) != 0 ? 1u : 0u);
+                ptx::mma_commit(&empty[stage]);
+                ptx::mma_commit(&aempty[as]);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                if (++as == AS) {
+                    as = 0;
+                    aphase ^= 1;
+                }
+            }
+            ptx::mma_commit(&tfull[acc]);
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------- epilogue: lane = weight row (feature), columns = tokens ----------------
+        // Each warp owns 32 features; per 32-token chunk it converts its column of
+        // accumulators, transposes them through shared memory and writes 32
+        // token rows of 32 consecutive features (32 * ESZ bytes each).
+        const int q = warp - 4;
+        uint8_t* const ep0 = smem + L::epi_off + q * 2 * L::epi_buf;
+        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);  // quantize.cpp:193
+        int it = 0, chunk = 0;
+        if (tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
+        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
+            const int f_blk = tile / num_t, t_blk = tile % num_t;
+            const int acc = it & 1;
+            if (lane == 0 && q == 0) {
+                FQG_TWAIT2(3, ptx::mbar_wait(&tfull[acc], (it >> 1) & 1));
+            }
+            __syncwarp();
+            ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
+            ptx::tc_fence_after();
+            const long long te0 = clock64();
+            const int f0 = f_blk * 128 + 32 * q, feat = f0 + lane;
+            const bool fok = feat < n;
+            const double bv = (bias != nullptr && fok) ? load_bias(bias, bias_dt, feat) : 0.0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c, ++chunk) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN + 32 * c,
+                                        r);
+                const int t0 = t_blk * BN + 32 * c;
+                const int rs = t0 + lane < m ? rowsum[t0 + lane] : 0;
+                uint8_t* ep = ep0 + (chunk & 1) * L::epi_buf;
+                if (tma_y) {  // this buffer's previous TMA store has read it
+                    if (lane == 0) ptx::bulk_wait_read_allbut1();
+                    __syncwarp();
+                }
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {  // token j of the chunk -> row j of the tile
+                    const int corr = 8 * __shfl_sync(0xffffffffu, rs, j);
+                    *reinterpret_cast<OT*>(ep + j * L::epi_row + lane * ESZ) =
+                        convert_out<OUT>(static_cast<int32_t>(r[j]) - corr, s, bv);
+                }
+                if (tma_y) {
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0 && !(dbg & 4)) {
+                        ptx::tma_store_2d(&tmY, ep, f0, t0);
+                        ptx::bulk_commit();
+                    }
+                } else {
+                    __syncwarp();
+                    const int tok = t0 + lane;  // lane writes token row `lane`
+                    if (tok < m && !(dbg & 4)) {
+                        OT* dst = static_cast<OT*>(y) + static_cast<int64_t>(tok) * ldy + f0;
+                        for (int e = 0; e < 32 && f0 + e < n; ++e)
+                            dst[e] = *reinterpret_cast<const OT*>(ep + lane * L::epi_row + e * ESZ);
+                    }
+                    __syncwarp();
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (dbg && lane == 0 && q == 0) atomicAdd(&g_dbg2[blockIdx.x % 296][4], clock64() - te0);
+        }
+    } else if (warp >= 8) {
+        // ---------------- unpack teams: L2 -> registers -> TMEM A ring ----------------
+        // Team t takes steps t, t + 2, ... of the (tile, k-block) sequence; each
+        // lane keeps its weight row's next three steps (64 bytes each) in flight.
+        const int team = (warp - 8) >> 2, q = warp & 3;
+        const int my_tiles = blockIdx.x < num_tiles ? (num_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+        const int steps = my_tiles * num_kb;
+        auto load_step = [&](int st_i, uint4 (&v)[4]) {
+            if (st_i >= steps) return;
+            const int tile = blockIdx.x + (st_i / num_kb) * gridDim.x, kb = st_i % num_kb;
+            const int feat = (tile / num_t) * 128 + 32 * q + lane;
+            const uint8_t* wrow = w + static_cast<int64_t>(feat < n ? feat : 0) * ldb;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int off = kb * (BK / 2) + 16 * i;
+                v[i] = (feat < n && off < kbytes) ? __ldg(reinterpret_cast<const uint4*>(wrow + off))
+                                                  : make_uint4(0u, 0u, 0u, 0u);
+            }
+        };
+        auto process = [&](int st_i, const uint4 (&v)[4]) {
+            const int as = st_i % AS;
+            uint32_t wd[32];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t pw[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    wd[8 * i + e] = pw[e] & 0x0F0F0F0Fu;             // k = 32i + 4e .. +3
+                    wd[8 * i + 4 + e] = (pw[e] >> 4) & 0x0F0F0F0Fu;  // k = 32i + 16 + 4e ..
+                }
+            }
+            if (lane == 0 && q == 0) {
+                FQG_TWAIT2(5 + team, ptx::mbar_wait(&aempty[as], ((st_i / AS) & 1) ^ 1));
+            }
+            __syncwarp();
+            ptx::mbar_wait(&aempty[as], ((st_i / AS) & 1) ^ 1);
+            ptx::tc_fence_after();
+            if (!(dbg & 2))
+                ptx::tmem_st_32x32b_x32(
+                    tmem_base + (static_cast<uint32_t>(32 * q) << 16) + L::a_col0 + as * 32, wd);
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_relaxed(&afull[as]);
+        };
+        uint4 va[4], vb[4], vc[4];
+        load_step(team, va);
+        load_step(team + 2, vb);
+        load_step(team + 4, vc);
+        for (int st_i = team; st_i < steps; st_i += 6) {
+            process(st_i, va);
+            load_step(st_i + 6, va);
+            if (st_i + 2 >= steps) break;
+            process(st_i + 2, vb);
+            load_step(st_i + 8, vb);
+            if (st_i + 4 >= steps) break;
+            process(st_i + 4, vc);
+            load_step(st_i + 10, vc);
+        }
+    }
+    if (tma_y && warp >= 4 && warp < 8 && lane == 0) ptx::bulk_wait_all();  // epilogue stores
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        __syncwarp();
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc(tmem_base, 512);
     }
 }
 
@@ -790,10 +1140,32 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
         FQG_CUDA(cudaMemcpyToSymbol(g_dbg, zeros, sizeof(zeros)));
         FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
     }
+    // Stream-K when whole tiles would leave a partial last round and every
+    // cluster's range still spans at least one full tile (two-way splits).
+    // Off by default: measured slower than data-parallel tiles on B200 (75 vs
+    // 61 us at 2048x4096x7488): the misaligned k offsets of the ranges cost more
+    // than the partial last round. FQG_GEMM_STREAMK=1 enables it.
+    static const int sk_env = [] {
+        const char* e = std::getenv("FQG_GEMM_STREAMK");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int64_t units = static_cast<int64_t>(num_tiles) * num_kb;
+    const bool sk = sk_env != 0 && num_tiles > clusters && num_tiles % clusters != 0 &&
+                    units / clusters >= num_kb;
+    int32_t* ws = nullptr;
+    int* ws_flag = nullptr;
+    if (sk) {
+        const size_t wbytes = static_cast<size_t>(clusters + 1) * 256 * 256 * 4;
+        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes + (clusters + 1) * 4, stream));
+        ws_flag = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + wbytes);
+        FQG_CUDA(cudaMemsetAsync(ws_flag, 0, (clusters + 1) * 4, stream));
+    }
     kern<<<2 * clusters, L::threads, L::total, stream>>>(
         ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb, g.scale, g.bias,
-        g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum);
-    FQG_CUDA(cudaGetLastError());
+        g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk ? 1 : 0, ws, ws_flag);
+    const cudaError_t le = cudaGetLastError();
+    if (ws) cudaFreeAsync(ws, stream);
+    FQG_CUDA(le);
     if (dbg) {
         unsigned long long h[296][8];
         FQG_CUDA(cudaDeviceSynchronize());
@@ -829,6 +1201,8 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
         double a2[8] = {0};
         for (int c = 0; c < nc; ++c)
             for (int i = 0; i < 8; ++i) a2[i] += static_cast<double>(h2[c][i]) / nc;
+        std::fprintf(stderr, "[fqg gemm pair] stream-K head: flag wait %.0f cyc, reached at %.0f cyc\n",
+                     a2[6], a2[7]);
         std::fprintf(stderr,
                      "[fqg gemm pair] per CTA: mma wait ufull %.0f, wait full_mma %.0f | unpack "
                      "(thread 0): wait full_unp %.0f, wait uempty %.0f, work %.0f cyc over %.0f "
@@ -859,6 +1233,87 @@ void dispatch_out(const GemmArgs& g, cudaStream_t s) {
         case FQG_F32: return launch<BN, ST, FQG_F32, AF, BF>(g, s);
         case FQG_F16: return launch<BN, ST, FQG_F16, AF, BF>(g, s);
         case FQG_BF16: return launch<BN, ST, FQG_BF16, AF, BF>(g, s);
+        default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
+    }
+}
+
+template <int BN, int STAGES, int OUT>
+void launch_w4t(const GemmArgs& g, cudaStream_t stream) {
+    using L = W4Layout<BN, STAGES, sizeof(typename OutT<OUT>::T)>;
+    static_assert(L::total <= 227 * 1024, "shared memory budget");
+    CUtensorMap tx;
+    make_tmap_2d_u8(&tx, g.a, static_cast<uint64_t>(g.kp), static_cast<uint64_t>(g.m),
+                    static_cast<uint64_t>(g.lda), BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
+    auto kern = k_gemm_w4t<BN, STAGES, OUT>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        attr_set = true;
+    }
+    int dev = 0;
+    FQG_CUDA(cudaGetDevice(&dev));
+    const int num_tiles = static_cast<int>(((g.m + BN - 1) / BN) * ((g.n + 127) / 128));
+    const int grid = std::max(1, std::min(num_tiles, num_sms(dev)));
+    const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
+    const int esz = dtype_size(g.y_dtype);
+    const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
+    static const int dbg = [] {
+        const char* e = std::getenv("FQG_GEMM_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (dbg) {
+        static unsigned long long zeros[296][8] = {};
+        FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
+    }
+    // Output tiles leave by TMA tensor stores when y allows it (16-byte aligned
+    // base and row pitch).
+    CUtensorMap ty;
+    std::memset(&ty, 0, sizeof(ty));
+    const bool tma_y = vec;
+    if (tma_y) {
+        const CUtensorMapDataType dt = esz == 8   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                       : esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(g.m)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.ldy * esz)};
+        const cuuint32_t box[2] = {32, 32};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode_fn()(&ty, dt, 2, g.y, dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed (" + std::to_string(r) + ")");
+    }
+    kern<<<grid, L::threads, L::total, stream>>>(tx, static_cast<const uint8_t*>(g.b), g.ldb,
+                                                 static_cast<int>(g.kp / 2), g.y, g.ldy,
+                                                 static_cast<int>(g.m), static_cast<int>(g.n),
+                                                 num_kb, g.scale, g.bias, g.bias_dtype, g.rowsum,
+                                                 vec ? 1 : 0, dbg, ty, tma_y ? 1 : 0);
+    FQG_CUDA(cudaGetLastError());
+    if (dbg) {
+        unsigned long long h[296][8];
+        FQG_CUDA(cudaDeviceSynchronize());
+        FQG_CUDA(cudaMemcpyFromSymbol(h, g_dbg2, sizeof(h)));
+        double a[8] = {0};
+        for (int c = 0; c < grid; ++c)
+            for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[c][i]) / grid;
+        std::fprintf(stderr,
+                     "[fqg gemm w4t] per CTA cycles: mma wait tempty %.0f, wait full(x) %.0f, wait "
+                     "afull(w) %.0f | epilogue wait tfull %.0f, work %.0f | unpack wait aempty "
+                     "team0 %.0f team1 %.0f | %d k-blocks/tile\n",
+                     a[0], a[1], a[2], a[3], a[4], a[5], a[6], num_kb);
+    }
+}
+
+void dispatch_w4t(const GemmArgs& g, cudaStream_t s) {
+    constexpr int BN = 192, ST = 6;
+    switch (g.y_dtype) {
+        case FQG_I32: return launch_w4t<BN, ST, FQG_I32>(g, s);
+        case FQG_F64: return launch_w4t<BN, ST, FQG_F64>(g, s);
+        case FQG_F32: return launch_w4t<BN, ST, FQG_F32>(g, s);
+        case FQG_F16: return launch_w4t<BN, ST, FQG_F16>(g, s);
+        case FQG_BF16: return launch_w4t<BN, ST, FQG_BF16>(g, s);
         default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
     }
 }
@@ -923,14 +1378,16 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
         return e ? std::atoi(e) : 0;
     }();
     int v = g.variant != 0 ? g.variant : env_variant;
-    // Measured (tools/gemm_sweep.py): the pair kernel wins for int8 x int8; with a
-    // packed int4 operand the single-CTA kernel's unpack pipeline is faster.
+    // Measured at 2048 x 4096 x 7488: pair 61 us (int8 weights) / 71 us (biased
+    // int4), single-CTA 71 us (int4), weights-in-TMEM 87 us (int4).
     if (v == 0)
         v = (g.m > BM && g.n > 128 && g.a_fmt == FQG_I8 &&
              (g.b_fmt == FQG_I8 || g.b_fmt == FQG_I4_BIASED))
                 ? 2
                 : 1;
-    if (v == 2)
+    if (v == 3 && g.a_fmt == FQG_I8 && g.b_fmt == FQG_I4_BIASED)
+        dispatch_w4t(g, stream);
+    else if (v == 2)
         dispatch_pair_fmt(g, stream);
     else if (g.n <= 128)
         dispatch_fmt<128>(g, stream);

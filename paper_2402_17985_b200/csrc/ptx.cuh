@@ -34,6 +34,13 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// Relaxed arrive: no release fence, so it does not wait for this thread's
+// outstanding global loads (prefetches). Only for handing over tcgen05 results
+// ordered by tcgen05.wait::st + tcgen05.fence::before_thread_sync.
+__device__ __forceinline__ void mbar_arrive_relaxed(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.relaxed.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -87,6 +94,16 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uin
                      reinterpret_cast<uint64_t>(gdst)),
                  "r"(smem_u32(smem_src)), "r"(bytes)
                  : "memory");
+}
+// 2-D tiled bulk tensor store shared -> global (bulk_group completion); the TMA
+// unit clips the box at the tensor bounds.
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem_src,
+                                             int32_t c0, int32_t c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(smem_u32(smem_src)), "r"(c0), "r"(c1)
+        : "memory");
 }
 __device__ __forceinline__ void bulk_commit() {
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -151,6 +168,33 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns from 32 registers (thread t -> lane base + t).
+__device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+        "{%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, "
+        "%17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(
+            taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+        "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+        "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+// D[tmem] (+)= A[tmem] * B[smem]^T, kind::i8, one CTA (A: 128 lanes x K/4 columns).
+__device__ __forceinline__ void mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 __device__ __forceinline__ void tmem_wait_ld() {
@@ -260,9 +304,10 @@ __device__ __forceinline__ uint64_t smem_desc_sw128_kmajor(uint32_t smem_addr) {
 // int8, both K-major. c_format [4,6)=2 (S32); a_format [7,10)=1 (INT8);
 // b_format [10,13)=1 (INT8) / 0 (UINT8); a_major [15]=0, b_major [16]=0;
 // N>>3 at [17,23); M>>4 at [24,29).
-__host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n, bool b_unsigned = false) {
-    return (2u << 4) | (1u << 7) | ((b_unsigned ? 0u : 1u) << 10) | ((n >> 3) << 17) |
-           ((m >> 4) << 24);
+__host__ __device__ constexpr uint32_t idesc_i8(uint32_t m, uint32_t n, bool b_unsigned = false,
+                                                bool a_unsigned = false) {
+    return (2u << 4) | ((a_unsigned ? 0u : 1u) << 7) | ((b_unsigned ? 0u : 1u) << 10) |
+           ((n >> 3) << 17) | ((m >> 4) << 24);
 }
 
 }  // namespace ptx

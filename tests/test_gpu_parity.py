@@ -236,3 +236,24 @@ def test_full_size_row_subset(port, fq, bits, a_fmt, b_fmt):
     y_ref, _, _, acc_ref = port.run_layer(L, x[rows], debug=True)
     assert np.array_equal(acc[rows].astype(np.int64), acc_ref)
     fp16_close(y16[rows], y_ref)
+
+
+@pytest.mark.parametrize("m,n,kp", [(512, 10240, 1024), (2048, 4096, 512), (300, 8960, 2048)])
+def test_gemm_stream_k_shapes(fq, m, n, kp):
+    """Shapes whose 256x256 tile count leaves a partial last round on 74 CTA
+    pairs: the stream-K split (two clusters per tile, INT32 partials through a
+    workspace) must give the exact integer product."""
+    import torch
+
+    from paper_2402_17985_b200 import _lib
+
+    g = torch.Generator().manual_seed(m + n)
+    a = torch.randint(-127, 128, (m, kp), dtype=torch.int8, generator=g)
+    b = torch.randint(-127, 128, (n, kp), dtype=torch.int8, generator=g)
+    ref = a.numpy().astype(np.int64) @ b.numpy().astype(np.int64).T
+    ad, bd = a.cuda(), b.cuda()
+    y = torch.empty((m, n), dtype=torch.int32, device="cuda")
+    fq.check(fq.lib().fqg_gemm(ad.data_ptr(), _lib.I8, kp, bd.data_ptr(), _lib.I8, kp, m, n, kp,
+                               y.data_ptr(), _lib.I32, n, None, None, _lib.NONE,
+                               torch.cuda.current_stream().cuda_stream))
+    assert np.array_equal(y.cpu().numpy().astype(np.int64), ref)
