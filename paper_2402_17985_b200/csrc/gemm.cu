@@ -1058,6 +1058,265 @@ __global__ void __launch_bounds__(512, 1)
     }
 }
 
+// ------------------------------------------------------------------------
+// CTA-pair weights-in-TMEM kernel (biased int4 weights): a cluster of 2 CTAs
+// computes a 256-feature x BN-token tile with tcgen05.mma.cta_group::2, A (the
+// weights, 128 rows per CTA) read from each CTA's TENSOR memory, B (the
+// activation tile, BN/2 token rows per CTA) from SMEM via 2-SM TMA. Each CTA's
+// unpack teams fill only their own TMEM (no cross-CTA data), arriving on the
+// leader's barrier; the epilogue (per CTA: its 128 features) transposes
+// through SMEM and leaves by TMA tensor stores.
+template <int BN, int STAGES, int ESZ, int NACC = 2>
+struct W4PairLayout {
+    static constexpr int b_half = (BN / 2) * BK;  // this CTA's token rows x 128 bytes
+    static constexpr int epi_row = 32 * ESZ;
+    static constexpr int epi_buf = 32 * epi_row;
+    static constexpr int epi_off = STAGES * b_half;
+    static constexpr int bar_off = epi_off + 4 * 2 * epi_buf;
+    static constexpr int n_bars = 2 * STAGES + 2 * kW4AStages + 4;
+    static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
+    static constexpr int threads = 512;
+    // NACC accumulators (2: the epilogue of tile i overlaps tile i + 1; 1: N = 256
+    // tokens, the largest and fastest MMA shape, epilogue drains before reuse)
+    static constexpr uint32_t a_col0 = NACC * BN;
+    static_assert(NACC * BN + 32 * kW4AStages <= 512, "TMEM budget");
+    static_assert(BN % 32 == 0 && (BN / 2) % 8 == 0, "token tile");
+};
+
+template <int BN, int STAGES, int OUT, int NACC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
+    k_gemm_w4t_pair(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w,
+                    int64_t ldb, int kbytes, void* __restrict__ y, int64_t ldy, int m, int n,
+                    int num_kb, const double* __restrict__ scale, const void* __restrict__ bias,
+                    int bias_dt, const int32_t* __restrict__ rowsum,
+                    const __grid_constant__ CUtensorMap tmY, int tma_y, int dbg) {
+    const long long t_start = clock64();
+    using OT = typename OutT<OUT>::T;
+    constexpr int ESZ = sizeof(OT);
+    using L = W4PairLayout<BN, STAGES, ESZ, NACC>;
+    constexpr int AS = kW4AStages;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);  // leader: both B halves
+    uint64_t* empty = full + STAGES;                                   // own: B stage free
+    uint64_t* afull = empty + STAGES;                                  // leader: A stage (both)
+    uint64_t* aempty = afull + AS;                                     // own: A stage free
+    uint64_t* tfull = aempty + AS;                                     // own: accumulator ready
+    uint64_t* tempty = tfull + 2;                                      // leader: drained (both)
+    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    const int num_t = (m + BN - 1) / BN, num_f = (n + 255) / 256;
+    const int num_tiles = num_t * num_f;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    if (threadIdx.x == 0) {
+        ptx::tma_prefetch_desc(&tmX);
+        for (int i = 0; i < STAGES; ++i) {
+            ptx::mbar_init(&full[i], 1);
+            ptx::mbar_init(&empty[i], 1);
+        }
+        for (int i = 0; i < AS; ++i) {
+            ptx::mbar_init(&afull[i], 8);  // one team's 4 warps in both CTAs
+            ptx::mbar_init(&aempty[i], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 8);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc_pair(tmem_holder, 512);
+        ptx::tmem_relinquish_pair();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_holder;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer (both CTAs): own token half ----------------
+        const uint64_t keep = ptx::policy_evict_last();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            const int t_row = (tile % num_t) * BN + static_cast<int>(rank) * (BN / 2);
+            for (int kb = 0; kb < num_kb; ++kb) {
+                ptx::mbar_wait(&empty[stage], phase ^ 1);
+                if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * L::b_half);
+                ptx::tma_load_2d_2sm(smem + stage * L::b_half, &tmX,
+                                     ptx::mapa(ptx::smem_u32(&full[stage]), 0), kb * BK, t_row, keep);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ---------------- MMA issuer (leader) ----------------
+        constexpr uint32_t idesc = ptx::idesc_i8(256, BN, /*b_unsigned=*/false, /*a_unsigned=*/true);
+        int stage = 0, as = 0, it = 0;
+        uint32_t phase = 0, aphase = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+            const int acc = it % NACC;
+            FQG_TWAIT2(0, ptx::mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1));
+            ptx::tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int kb = 0; kb < num_kb; ++kb) {
+                FQG_TWAIT2(1, ptx::mbar_wait(&full[stage], phase));
+                FQG_TWAIT2(2, ptx::mbar_wait(&afull[as], aphase));
+                ptx::tc_fence_after();
+                const uint32_t a_tmem = tmem_base + L::a_col0 + as * 32;
+                const uint32_t b_addr = ptx::smem_u32(smem + stage * L::b_half);
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k)
+                    ptx::mma_i8_ts_pair(d_tmem, a_tmem + k * (UK / 4),
+                                        ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
+                                        (kb | k) != 0 ? 1u : 0u);
+                ptx::mma_commit_pair(&empty[stage], 0x3);
+                ptx::mma_commit_pair(&aempty[as], 0x3);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+                if (++as == AS) {
+                    as = 0;
+                    aphase ^= 1;
+                }
+            }
+            ptx::mma_commit_pair(&tfull[acc], 0x3);
+        }
+        if (dbg) atomicAdd(&g_dbg2[blockIdx.x % 296][3], clock64() - t_start);
+    } else if (warp >= 4 && warp < 8) {
+        // ---------------- epilogue (both CTAs): lane = feature, columns = tokens ----------------
+        const int q = warp - 4;
+        uint8_t* const ep0 = smem + L::epi_off + q * 2 * L::epi_buf;
+        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);  // quantize.cpp:193
+        int it = 0, chunk = 0;
+        if (tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
+        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
+            const int f_blk = tile / num_t, t_blk = tile % num_t;
+            const int acc = it % NACC;
+            ptx::mbar_wait(&tfull[acc], (it / NACC) & 1);
+            ptx::tc_fence_after();
+            const int f0 = f_blk * 256 + static_cast<int>(rank) * 128 + 32 * q, feat = f0 + lane;
+            const bool fok = feat < n;
+            const double bv = (bias != nullptr && fok) ? load_bias(bias, bias_dt, feat) : 0.0;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c, ++chunk) {
+                uint32_t r[32];
+                if (!(dbg & 4))
+                    ptx::tmem_ld_32x32b_x32(
+                        tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN + 32 * c, r);
+                const int t0 = t_blk * BN + 32 * c;
+                const int rs = t0 + lane < m ? rowsum[t0 + lane] : 0;
+                uint8_t* ep = ep0 + (chunk & 1) * L::epi_buf;
+                if (tma_y) {
+                    if (lane == 0) ptx::bulk_wait_read_allbut1();
+                    __syncwarp();
+                }
+                ptx::tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const int corr = 8 * __shfl_sync(0xffffffffu, rs, j);
+                    *reinterpret_cast<OT*>(ep + j * L::epi_row + lane * ESZ) =
+                        convert_out<OUT>(static_cast<int32_t>(r[j]) - corr, s, bv);
+                }
+                if (tma_y) {
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&tmY, ep, f0, t0);
+                        ptx::bulk_commit();
+                    }
+                } else {
+                    __syncwarp();
+                    const int tok = t0 + lane;
+                    if (tok < m) {
+                        OT* dst = static_cast<OT*>(y) + static_cast<int64_t>(tok) * ldy + f0;
+                        for (int e = 0; e < 32 && f0 + e < n; ++e)
+                            dst[e] = *reinterpret_cast<const OT*>(ep + lane * L::epi_row + e * ESZ);
+                    }
+                    __syncwarp();
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+        }
+        if (tma_y && lane == 0) ptx::bulk_wait_all();
+        if (dbg && lane == 0 && q == 0) atomicAdd(&g_dbg2[blockIdx.x % 296][4], clock64() - t_start);
+    } else if (warp >= 8) {
+        // ---------------- unpack teams (both CTAs): L2 -> registers -> own TMEM ----------------
+        const int team = (warp - 8) >> 2, q = warp & 3;
+        const int my_tiles = cid < num_tiles ? (num_tiles - 1 - cid) / ncl + 1 : 0;
+        const int steps = my_tiles * num_kb;
+        const uint32_t lead_afull = ptx::mapa(ptx::smem_u32(afull), 0);
+        auto load_step = [&](int st_i, uint4 (&v)[4]) {
+            if (st_i >= steps) return;
+            const int tile = cid + (st_i / num_kb) * ncl, kb = st_i % num_kb;
+            const int feat = (tile / num_t) * 256 + static_cast<int>(rank) * 128 + 32 * q + lane;
+            const uint8_t* wrow = w + static_cast<int64_t>(feat < n ? feat : 0) * ldb;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int off = kb * (BK / 2) + 16 * i;
+                v[i] = (feat < n && off < kbytes) ? __ldg(reinterpret_cast<const uint4*>(wrow + off))
+                                                  : make_uint4(0u, 0u, 0u, 0u);
+            }
+        };
+        auto process = [&](int st_i, const uint4 (&v)[4]) {
+            const int as = st_i % AS;
+            uint32_t wd[32];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t pw[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    wd[8 * i + e] = pw[e] & 0x0F0F0F0Fu;             // k = 32i + 4e .. +3
+                    wd[8 * i + 4 + e] = (pw[e] >> 4) & 0x0F0F0F0Fu;  // k = 32i + 16 + 4e ..
+                }
+            }
+            if (dbg && lane == 0 && q == 0) {
+                FQG_TWAIT2(5 + team, ptx::mbar_wait(&aempty[as], ((st_i / AS) & 1) ^ 1));
+            }
+            __syncwarp();
+            ptx::mbar_wait(&aempty[as], ((st_i / AS) & 1) ^ 1);
+            ptx::tc_fence_after();
+            if (!(dbg & 2))
+                ptx::tmem_st_32x32b_x32(
+                    tmem_base + (static_cast<uint32_t>(32 * q) << 16) + L::a_col0 + as * 32, wd);
+            ptx::tmem_wait_st();
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(lead_afull + as * 8);
+        };
+        uint4 va[4], vb[4], vc[4];
+        load_step(team, va);
+        load_step(team + 2, vb);
+        load_step(team + 4, vc);
+        for (int st_i = team; st_i < steps; st_i += 6) {
+            process(st_i, va);
+            load_step(st_i + 6, va);
+            if (st_i + 2 >= steps) break;
+            process(st_i + 2, vb);
+            load_step(st_i + 8, vb);
+            if (st_i + 4 >= steps) break;
+            process(st_i + 4, vc);
+            load_step(st_i + 10, vc);
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        __syncwarp();
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair(tmem_base, 512);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -1318,6 +1577,85 @@ void dispatch_w4t(const GemmArgs& g, cudaStream_t s) {
     }
 }
 
+template <int BN, int STAGES, int OUT, int NACC>
+void launch_w4t_pair(const GemmArgs& g, cudaStream_t stream) {
+    using L = W4PairLayout<BN, STAGES, sizeof(typename OutT<OUT>::T), NACC>;
+    static_assert(L::total <= 227 * 1024, "shared memory budget");
+    CUtensorMap tx;
+    make_tmap_2d_u8(&tx, g.a, static_cast<uint64_t>(g.kp), static_cast<uint64_t>(g.m),
+                    static_cast<uint64_t>(g.lda), BK, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B);
+    auto kern = k_gemm_w4t_pair<BN, STAGES, OUT, NACC>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
+        attr_set = true;
+    }
+    int dev = 0;
+    FQG_CUDA(cudaGetDevice(&dev));
+    const int num_tiles = static_cast<int>(((g.m + BN - 1) / BN) * ((g.n + 255) / 256));
+    const int clusters = std::max(1, std::min(num_tiles, num_sms(dev) / 2));
+    const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
+    const int esz = dtype_size(g.y_dtype);
+    const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
+    CUtensorMap ty;
+    std::memset(&ty, 0, sizeof(ty));
+    if (vec) {
+        const CUtensorMapDataType dt = esz == 8   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                       : esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(g.m)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.ldy * esz)};
+        const cuuint32_t box[2] = {32, 32};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode_fn()(&ty, dt, 2, g.y, dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed (" + std::to_string(r) + ")");
+    }
+    static const int dbg = [] {
+        const char* e = std::getenv("FQG_GEMM_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (dbg) {
+        static unsigned long long zeros[296][8] = {};
+        FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
+    }
+    kern<<<2 * clusters, L::threads, L::total, stream>>>(
+        tx, static_cast<const uint8_t*>(g.b), g.ldb, static_cast<int>(g.kp / 2), g.y, g.ldy,
+        static_cast<int>(g.m), static_cast<int>(g.n), num_kb, g.scale, g.bias, g.bias_dtype,
+        g.rowsum, ty, vec ? 1 : 0, dbg);
+    FQG_CUDA(cudaGetLastError());
+    if (dbg) {
+        unsigned long long h[296][8];
+        FQG_CUDA(cudaDeviceSynchronize());
+        FQG_CUDA(cudaMemcpyFromSymbol(h, g_dbg2, sizeof(h)));
+        double a[8] = {0};
+        for (int c = 0; c < 2 * clusters; ++c)
+            for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[c][i]) / (2 * clusters);
+        std::fprintf(stderr,
+                     "[fqg gemm w4t_pair] per CTA cycles (leader-only x2): mma wait tempty %.0f, "
+                     "full(x) %.0f, afull(w) %.0f, mma loop end %.0f | epilogue end %.0f | unpack "
+                     "wait aempty %.0f / %.0f | tiles %d, k-blocks %d\n",
+                     2 * a[0], 2 * a[1], 2 * a[2], 2 * a[3], a[4], a[5], a[6], num_tiles, num_kb);
+    }
+}
+
+// Pair tile 256 features x 256 tokens, one accumulator (MMA 256x256x32 in TS
+// mode: 4563 TOPS measured vs 2900 at N = 160, tools/mma_ts.cu).
+void dispatch_w4t_pair(const GemmArgs& g, cudaStream_t s) {
+    constexpr int BN = 256, ST = 8, NA = 1;
+    switch (g.y_dtype) {
+        case FQG_I32: return launch_w4t_pair<BN, ST, FQG_I32, NA>(g, s);
+        case FQG_F64: return launch_w4t_pair<BN, ST, FQG_F64, NA>(g, s);
+        case FQG_F32: return launch_w4t_pair<BN, ST, FQG_F32, NA>(g, s);
+        case FQG_F16: return launch_w4t_pair<BN, ST, FQG_F16, NA>(g, s);
+        case FQG_BF16: return launch_w4t_pair<BN, ST, FQG_BF16, NA>(g, s);
+        default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
+    }
+}
+
 int kfmt(int f) { return f == FQG_I8 ? F8 : (f == FQG_I4 ? FS4 : FU4); }
 
 void dispatch_pair_fmt(const GemmArgs& g, cudaStream_t s) {
@@ -1387,6 +1725,8 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
                 : 1;
     if (v == 3 && g.a_fmt == FQG_I8 && g.b_fmt == FQG_I4_BIASED)
         dispatch_w4t(g, stream);
+    else if (v == 4 && g.a_fmt == FQG_I8 && g.b_fmt == FQG_I4_BIASED)
+        dispatch_w4t_pair(g, stream);
     else if (v == 2)
         dispatch_pair_fmt(g, stream);
     else if (g.n <= 128)
