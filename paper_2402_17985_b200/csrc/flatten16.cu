@@ -39,6 +39,8 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 
 #include "fqg_internal.h"
@@ -142,24 +144,28 @@ __device__ __forceinline__ uint32_t pack_i4_word(uint32_t lo, uint32_t hi) {
     return (lo & 0x0F0F0F0Fu) | ((hi << 4) & 0xF0F0F0F0u);
 }
 
-// K1 layout: a CTA of kWarps row workers (one warp per token row) shares the
-// per-channel certificate in shared memory; each warp owns its final operand
-// row (+ a zero byte at column K' for padding copies), its int4 packing, a
-// tier-2 queue and a long-run list. x streams straight into registers
-// (16-byte loads, eight per lane per chunk, the next chunk in flight while
-// the current one is computed); finished rows leave by bulk stores.
-constexpr int kWarps = 8;     // row workers per CTA
-constexpr int kCh = 8;        // 16-byte x loads per lane per chunk (= 8 channel groups)
-constexpr int kInline = 6;    // extension runs up to this long are written by their lane
-constexpr int kRunCap = 64;   // longer runs are listed and written by the whole warp
-constexpr int kQCap = 128;    // tier-2 queue entries per warp
-constexpr int kHotRegs = 4;   // hot channels per lane (nhot <= 128)
+// K1 layout: a CTA of kWarps warps forms row teams of TW threads (TW / 32
+// warps, synchronised by a named barrier); each team streams its own token
+// rows. The CTA shares the per-channel certificate in shared memory; each team
+// owns its final operand row (+ a zero byte at column K' for padding copies),
+// its int4 packing, a tier-2 queue and a long-run list. x streams straight
+// into registers (16-byte loads, the next chunk in flight while the current
+// one is computed); finished rows leave by bulk stores. Splitting a row over
+// several warps shortens the per-row dependency chain, which (with all rows
+// in flight at once) is what bounds this kernel.
+constexpr int kWarps = 8;     // warps per CTA
+constexpr int kCh = 8;        // 16-byte x loads per thread per chunk (= 8 channel groups)
+constexpr int kInline = 6;    // extension runs up to this long are written by their thread
+constexpr int kRunCap = 32;   // longer runs are listed and written by the whole team
+constexpr int kQCap = 128;    // tier-2 queue entries per team
+constexpr int kMaxHot = 128;  // hot channels (layer.cu caps the list)
 
 struct K1Smem {
-    uint32_t cj, pj, per_warp0, fl, pk, queue, runs, per_warp, total;
+    uint32_t cj, pj, wsrc, hotm, hotg, tbar, per_team0, fl, pk, queue, runs, hotx, per_team, total;
+    uint32_t hotg_bytes;
     int ldf;
 };
-K1Smem k1_smem(int k, int kp, bool pack4) {
+K1Smem k1_smem(int k, int kp, int c1, bool pack4, int teams) {
     K1Smem w{};
     uint32_t o = 0;
     auto take = [&](uint32_t& at, uint32_t bytes) {
@@ -168,15 +174,21 @@ K1Smem k1_smem(int k, int kp, bool pack4) {
     };
     take(w.cj, static_cast<uint32_t>(k) * 4);
     take(w.pj, static_cast<uint32_t>(k) * 2);
-    w.per_warp0 = o;
+    take(w.wsrc, static_cast<uint32_t>(kp - c1) * 4);
+    take(w.hotm, kMaxHot * 16);
+    w.hotg_bytes = static_cast<uint32_t>((k / 8 + 3) / 4 * 16);
+    take(w.hotg, w.hotg_bytes);
+    take(w.tbar, 16);
+    w.per_team0 = o;
     w.ldf = kp + 16;
     o = 0;
     take(w.fl, static_cast<uint32_t>(w.ldf));
     take(w.pk, pack4 ? static_cast<uint32_t>(kp) / 2 : 0u);
     take(w.queue, kQCap * 8);
     take(w.runs, kRunCap * 16);
-    w.per_warp = o;
-    w.total = w.per_warp0 + kWarps * w.per_warp;
+    take(w.hotx, kMaxHot * 2);
+    w.per_team = o;
+    w.total = w.per_team0 + teams * w.per_team;
     return w;
 }
 
@@ -184,10 +196,13 @@ struct K16Params {
     const void* x;
     int64_t ldx;
     int m, k, kp, c1, ldf, nhot;
-    uint32_t s_cj, s_pj, per_warp0, fl, pk, queue, runs, per_warp;
+    uint32_t s_cj, s_pj, s_wsrc, s_hotm, s_hotg, s_tbar, hotg_bytes, per_team0, fl, pk, queue, runs,
+        hotx, per_team;
     const float* cj;
     const uint16_t* pj;
     const int32_t* hot;   // channels taking the exact path on every row (P_j = 0xFFFF)
+    const int32_t* hotm;  // [nhot] {j, cap, off, rs32 bits}
+    const int32_t* hotg;  // [k / 8] group hot mask | first hot index << 8
     const int32_t* off;   // [k] plan_x ext_offset
     const int32_t* wsrc;  // [kp - c1] flat column of each plan_w copy (padding -> kp, a zero byte)
     const double* s;
@@ -199,44 +214,54 @@ struct K16Params {
     int64_t ldq;
     unsigned long long* sat;
     int32_t* rowsum;
+    int dbg;
 };
 
-template <bool F16, bool PACK4>
+__device__ unsigned long long g_k1dbg[16];  // FQG_K1_DEBUG: summed phase end times (cycles)
+
+template <int TW>
+__device__ __forceinline__ void team_sync(int team) {
+    if constexpr (TW == 32)
+        __syncwarp();
+    else
+        asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(TW) : "memory");
+}
+
+template <bool F16, bool PACK4, int TW>
 __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_constant__ K16Params p) {
+    constexpr int TEAMS = kWarps * 32 / TW;
+    const long long t_start = clock64();
+    auto mark = [&](int slot) {
+        if (p.dbg && (threadIdx.x % TW) == 0) atomicAdd(&g_k1dbg[slot], clock64() - t_start);
+    };
     extern __shared__ __align__(16) uint8_t sm[];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int team = tid / TW, tt = tid % TW;
     const float* const scj = reinterpret_cast<const float*>(sm + p.s_cj);
     const uint16_t* const spj = reinterpret_cast<const uint16_t*>(sm + p.s_pj);
-    uint8_t* const base = sm + p.per_warp0 + warp * p.per_warp;
+    const int4* const swsrc = reinterpret_cast<const int4*>(sm + p.s_wsrc);
+    const int4* const shot = reinterpret_cast<const int4*>(sm + p.s_hotm);  // {j, cap, off, rs32}
+    const int32_t* const shotg = reinterpret_cast<const int32_t*>(sm + p.s_hotg);
+    uint8_t* const base = sm + p.per_team0 + team * p.per_team;
     int8_t* const fl = reinterpret_cast<int8_t*>(base + p.fl);
     uint8_t* const pk = base + p.pk;
     uint2* const queue = reinterpret_cast<uint2*>(base + p.queue);
     uint4* const runs = reinterpret_cast<uint4*>(base + p.runs);
-    __shared__ int qlen_s[kWarps], nrun_s[kWarps];
-    int& qlen = qlen_s[warp];
-    int& nrun = nrun_s[warp];
+    uint16_t* const hotx = reinterpret_cast<uint16_t*>(base + p.hotx);
+    __shared__ int qlen_s[TEAMS], nrun_s[TEAMS], rsum_s[TEAMS];
+    int& qlen = qlen_s[team];
+    int& nrun = nrun_s[team];
+    int& rsum_t = rsum_s[team];
 
     const int k = p.k, kp = p.kp, c1 = p.c1, ng_all = k >> 3;
     const SplitConsts& sc = p.sc;
     const int full = sc.qT;
-    const int worker = blockIdx.x * kWarps + warp, nworkers = gridDim.x * kWarps;
-    const int nch = (ng_all + 32 * kCh - 1) / (32 * kCh);  // chunks per row
+    const int worker = blockIdx.x * TEAMS + team, nworkers = gridDim.x * TEAMS;
+    const int nch = (ng_all + TW * kCh - 1) / (TW * kCh);  // chunks per row
     const int nrows_w = worker < p.m ? (p.m - 1 - worker) / nworkers + 1 : 0;
     const int nchunks = nrows_w * nch;
     const uint4* x4 = static_cast<const uint4*>(p.x);
     const int64_t ldx4 = p.ldx >> 3;
-
-    // stage the certificate (shared by the CTA's warps)
-    for (int i = threadIdx.x; i < (k >> 2); i += blockDim.x)
-        reinterpret_cast<float4*>(sm + p.s_cj)[i] = __ldg(reinterpret_cast<const float4*>(p.cj) + i);
-    for (int i = threadIdx.x; i < (k >> 3); i += blockDim.x)
-        reinterpret_cast<uint4*>(sm + p.s_pj)[i] = __ldg(reinterpret_cast<const uint4*>(p.pj) + i);
-    if (lane == 0) {
-        qlen = 0;
-        nrun = 0;
-        fl[kp] = 0;
-    }
-    __syncthreads();
 
     auto load_chunk = [&](uint4 (&buf)[kCh], int t) {
         if (t >= nchunks) return;
@@ -244,34 +269,56 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
         const uint4* src = x4 + static_cast<int64_t>(row) * ldx4;
 #pragma unroll
         for (int i = 0; i < kCh; ++i) {
-            const int g = (c * kCh + i) * 32 + lane;
+            const int g = (c * kCh + i) * TW + tt;
             if (g < ng_all) buf[i] = __ldg(src + g);
         }
     };
 
+    // the first x chunk is in flight while the tables are staged
+    uint4 xa[kCh], xb[kCh];
+    load_chunk(xa, 0);
+
+    // stage the per-layer tables (shared by the CTA's teams) with 1-D bulk copies
+    uint64_t* tbar = reinterpret_cast<uint64_t*>(sm + p.s_tbar);
+    if (tid == 0) {
+        ptx::mbar_init(tbar, 1);
+        ptx::fence_barrier_init();
+        const uint32_t b_cj = static_cast<uint32_t>(k) * 4, b_pj = static_cast<uint32_t>(k) * 2;
+        const uint32_t b_ws = static_cast<uint32_t>(kp - c1) * 4;
+        const uint32_t b_hm = static_cast<uint32_t>(p.nhot) * 16;
+        ptx::mbar_arrive_expect_tx(tbar, b_cj + b_pj + b_ws + b_hm + p.hotg_bytes);
+        ptx::bulk_load(sm + p.s_cj, p.cj, b_cj, tbar);
+        ptx::bulk_load(sm + p.s_pj, p.pj, b_pj, tbar);
+        if (b_ws) ptx::bulk_load(sm + p.s_wsrc, p.wsrc, b_ws, tbar);
+        if (b_hm) ptx::bulk_load(sm + p.s_hotm, p.hotm, b_hm, tbar);
+        ptx::bulk_load(sm + p.s_hotg, p.hotg, p.hotg_bytes, tbar);
+    }
+    if (tt == 0) {
+        qlen = 0;
+        nrun = 0;
+        rsum_t = 0;
+        fl[kp] = 0;
+    }
+    __syncthreads();
+    ptx::mbar_wait(tbar, 0);
+    mark(0);
+
     unsigned long long sat = 0;
-    uint32_t hx[kHotRegs];
-    // Row start: the previous row's bulk store has read fl / pk; zero the
+    // Row start: the team's previous bulk store has read fl / pk; zero the
     // plan_x extension slots [K, C1); fetch the hot channels' x values.
     auto row_begin = [&](int row) {
-        if (lane == 0) ptx::bulk_wait_read_all();
-        __syncwarp();
+        if (tt == 0) ptx::bulk_wait_read_all();
+        team_sync<TW>(team);
         const int z0 = (k + 15) & ~15;
-        if (z0 != k && lane == 0) *reinterpret_cast<uint2*>(fl + k) = make_uint2(0u, 0u);
-        for (int i = lane; i < (c1 - z0) >> 4; i += 32)
+        if (z0 != k && tt == 0) *reinterpret_cast<uint2*>(fl + k) = make_uint2(0u, 0u);
+        for (int i = tt; i < (c1 - z0) >> 4; i += TW)
             *reinterpret_cast<uint4*>(fl + z0 + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
-        const uint16_t* xr = static_cast<const uint16_t*>(p.x) + static_cast<int64_t>(row) * p.ldx;
-#pragma unroll
-        for (int i = 0; i < kHotRegs; ++i) {
-            const int h = lane + 32 * i;
-            hx[i] = h < p.nhot ? __ldg(xr + __ldg(p.hot + h)) : 0u;
-        }
     };
     // ---- tier 1 on one chunk: one FFMA per element; tier-2 elements are queued ----
     auto tier1 = [&](const uint4 (&buf)[kCh], int c) {
 #pragma unroll
         for (int i = 0; i < kCh; ++i) {
-            const int g = (c * kCh + i) * 32 + lane;
+            const int g = (c * kCh + i) * TW + tt;
             if (g >= ng_all) break;
             const float4 ca = reinterpret_cast<const float4*>(scj)[2 * g];
             const float4 cb = reinterpret_cast<const float4*>(scj)[2 * g + 1];
@@ -291,6 +338,16 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
             *reinterpret_cast<uint2*>(fl + 8 * g) =
                 make_uint2(pack_lowbytes(bq[0], bq[1], bq[2], bq[3]),
                            pack_lowbytes(bq[4], bq[5], bq[6], bq[7]));
+            if (const uint32_t hg = static_cast<uint32_t>(shotg[g]); (hg & 0xFFu) != 0u) {
+                uint32_t hm = hg & 0xFFu;  // hot channels of the group: keep their x for tier 2
+                int hi = static_cast<int>(hg >> 8);
+                while (hm != 0u) {
+                    const int e = __ffs(static_cast<int>(hm)) - 1;
+                    hm &= hm - 1u;
+                    const uint32_t wd = (e & 4) ? ((e & 2) ? xw.w : xw.z) : ((e & 2) ? xw.y : xw.x);
+                    hotx[hi++] = static_cast<uint16_t>(wd >> ((e & 1) << 4));
+                }
+            }
             const uint32_t all = tw[0] & tw[1] & tw[2] & tw[3] & 0x80008000u;
             if (all != 0x80008000u) {
                 uint32_t msk = ((~tw[0] >> 15) & 1u) | ((~tw[0] >> 30) & 2u) |
@@ -310,11 +367,10 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
             }
         }
     };
-    auto exact = [&](int j, uint32_t xb, int& ce, int& qe, int& fv, int& cap_e) {
+    auto exact = [&](int j, uint32_t xb, int cap_e, float rs32_j, int& ce, int& qe, int& fv) {
         const float xf = mag_to_f32<F16>(xb & 0x7FFFu) * ((xb & 0x8000u) ? -1.0f : 1.0f);
-        cap_e = __ldg(p.cap + j);
         const uint64_t res = split_quant_elem(xf, static_cast<double>(xf), p.s + j, p.rs + j,
-                                              __ldg(p.rs32 + j), cap_e, sc);
+                                              rs32_j, cap_e, sc);
         ce = static_cast<int>(res & 0xFFFF);
         qe = static_cast<int>(static_cast<int16_t>(res >> 16));
         fv = (res >> 32) & 1 ? -full : full;
@@ -322,16 +378,18 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
     };
     // Row end: tier 2, extension runs, plan_w copies, pack / sums, bulk store.
     auto row_end = [&](int row) {
-        __syncwarp();
+        mark(1);
+        team_sync<TW>(team);
         const int nq = qlen;
         const bool overflow = nq > kQCap;
         if (overflow) {  // pathological inputs: every non-hot tier-2 element inline
             const uint16_t* xr = static_cast<const uint16_t*>(p.x) + static_cast<int64_t>(row) * p.ldx;
-            for (int j = lane; j < k; j += 32) {
+            for (int j = tt; j < k; j += TW) {
                 const uint32_t xb = __ldg(xr + j);
                 if (spj[j] - (xb & 0x7FFFu) >= 0x8000u) continue;  // tier 1 or hot
-                int ce, qe, fv, cap_e;
-                exact(j, xb, ce, qe, fv, cap_e);
+                int ce, qe, fv;
+                const int cap_e = __ldg(p.cap + j);
+                exact(j, xb, cap_e, __ldg(p.rs32 + j), ce, qe, fv);
                 fl[j] = static_cast<int8_t>(ce >= 1 ? fv : qe);
                 const int last = ce >= 1 ? min(ce, cap_e - 1) : 0;
                 int8_t* ext = fl + k + __ldg(p.off + j) - 1;
@@ -339,65 +397,63 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
             }
         }
         const int nitems = p.nhot + (overflow ? 0 : nq);
-        for (int i0 = 0; i0 < nitems; i0 += 32) {
-            const int i = i0 + lane;
-            uint32_t xh = hx[0];
-#pragma unroll
-            for (int r = 1; r < kHotRegs; ++r)
-                if (i0 == 32 * r) xh = hx[r];
-            if (i < nitems) {
-                int j;
-                uint32_t xb;
-                if (i < p.nhot) {
-                    j = __ldg(p.hot + i);
-                    xb = xh;
-                } else {
-                    const uint2 e = queue[i - p.nhot];
-                    j = static_cast<int>(e.x);
-                    xb = e.y;
-                }
-                int ce, qe, fv, cap_e;
-                exact(j, xb, ce, qe, fv, cap_e);
-                fl[j] = static_cast<int8_t>(ce >= 1 ? fv : qe);  // slot j = piece 0
-                if (ce >= 1) {  // pieces 1 .. E -> the (zeroed) extension slots
-                    const int last = min(ce, cap_e - 1);
-                    const int ext0 = k + __ldg(p.off + j) - 1;
-                    int slot = kRunCap;
-                    if (last > kInline) slot = atomicAdd(&nrun, 1);
-                    if (slot < kRunCap)
-                        runs[slot] = make_uint4(static_cast<uint32_t>(ext0), static_cast<uint32_t>(last),
-                                                static_cast<uint32_t>(ce),
-                                                (static_cast<uint32_t>(fv) & 0xFFu) |
-                                                    ((static_cast<uint32_t>(qe) & 0xFFu) << 8));
-                    else
-                        for (int q = 1; q <= last; ++q)
-                            fl[ext0 + q] = static_cast<int8_t>(q < ce ? fv : qe);
-                }
+        for (int i = tt; i < nitems; i += TW) {
+            int j, cap_e, off_j;
+            float rs32_j;
+            uint32_t xb;
+            if (i < p.nhot) {
+                const int4 hm = shot[i];
+                j = hm.x, cap_e = hm.y, off_j = hm.z, rs32_j = __int_as_float(hm.w);
+                xb = hotx[i];
+            } else {
+                const uint2 e = queue[i - p.nhot];
+                j = static_cast<int>(e.x);
+                xb = e.y;
+                cap_e = __ldg(p.cap + j), off_j = __ldg(p.off + j), rs32_j = __ldg(p.rs32 + j);
+            }
+            int ce, qe, fv;
+            exact(j, xb, cap_e, rs32_j, ce, qe, fv);
+            fl[j] = static_cast<int8_t>(ce >= 1 ? fv : qe);  // slot j = piece 0
+            if (ce >= 1) {  // pieces 1 .. E -> the (zeroed) extension slots
+                const int last = min(ce, cap_e - 1);
+                const int ext0 = k + off_j - 1;
+                int slot = kRunCap;
+                if (last > kInline) slot = atomicAdd(&nrun, 1);
+                if (slot < kRunCap)
+                    runs[slot] = make_uint4(static_cast<uint32_t>(ext0), static_cast<uint32_t>(last),
+                                            static_cast<uint32_t>(ce),
+                                            (static_cast<uint32_t>(fv) & 0xFFu) |
+                                                ((static_cast<uint32_t>(qe) & 0xFFu) << 8));
+                else
+                    for (int q = 1; q <= last; ++q) fl[ext0 + q] = static_cast<int8_t>(q < ce ? fv : qe);
             }
         }
-        __syncwarp();
+        team_sync<TW>(team);
+        mark(2);
         const int nr = min(nrun, kRunCap);
-        for (int ri = 0; ri < nr; ++ri) {  // long runs: all lanes over one run's bytes
+        for (int ri = 0; ri < nr; ++ri) {  // long runs: the team over one run's bytes
             const uint4 rr = runs[ri];
             const int8_t v_full = static_cast<int8_t>(rr.w & 0xFFu);
             const int8_t v_rem = static_cast<int8_t>((rr.w >> 8) & 0xFFu);
-            for (int q = 1 + lane; q <= static_cast<int>(rr.y); q += 32)
+            for (int q = 1 + tt; q <= static_cast<int>(rr.y); q += TW)
                 fl[rr.x + q] = q < static_cast<int>(rr.z) ? v_full : v_rem;
         }
-        __syncwarp();
-        if (lane == 0) qlen = 0, nrun = 0;
+        team_sync<TW>(team);
+        if (tt == 0) qlen = 0, nrun = 0;
+        mark(3);
         // plan_w copies [C1, K'): byte gathers from the flattened row
-        for (int u = lane; u < ((kp - c1) >> 2); u += 32) {
-            const int4 sv = __ldg(reinterpret_cast<const int4*>(p.wsrc) + u);
+#pragma unroll 4
+        for (int u = tt; u < ((kp - c1) >> 2); u += TW) {
+            const int4 sv = swsrc[u];
             const uint32_t b0 = static_cast<uint8_t>(fl[sv.x]), b1 = static_cast<uint8_t>(fl[sv.y]);
             const uint32_t b2 = static_cast<uint8_t>(fl[sv.z]), b3 = static_cast<uint8_t>(fl[sv.w]);
             *reinterpret_cast<uint32_t*>(fl + c1 + 4 * u) =
                 __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
         }
         if (PACK4 || p.rowsum != nullptr) {
-            __syncwarp();
+            team_sync<TW>(team);
             int rsum = 0;
-            for (int u = lane; u < (kp >> 5); u += 32) {
+            for (int u = tt; u < (kp >> 5); u += TW) {
                 const uint4 lo = *reinterpret_cast<const uint4*>(fl + 32 * u);
                 const uint4 hi = *reinterpret_cast<const uint4*>(fl + 32 * u + 16);
                 rsum = __dp4a(static_cast<int>(lo.x), 0x01010101, rsum);
@@ -416,28 +472,32 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
             if (p.rowsum != nullptr) {
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-                if (lane == 0) p.rowsum[row] = rsum;
+                if (lane == 0) atomicAdd(&rsum_t, rsum);
             }
         }
         ptx::fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
+        team_sync<TW>(team);
+        mark(4);
+        if (tt == 0) {
             ptx::bulk_store(p.q + static_cast<int64_t>(row) * p.ldq,
                             PACK4 ? static_cast<const void*>(pk) : static_cast<const void*>(fl),
                             PACK4 ? static_cast<uint32_t>(kp >> 1) : static_cast<uint32_t>(kp));
             ptx::bulk_commit();
+            if (p.rowsum != nullptr) {
+                p.rowsum[row] = rsum_t;
+                rsum_t = 0;  // next use is after this team's next row_begin barrier
+            }
         }
     };
     auto step = [&](const uint4 (&buf)[kCh], int t) {
         const int row = worker + (t / nch) * nworkers, c = t % nch;
         if (c == 0) row_begin(row);
+        if (c == 0) mark(7);
         tier1(buf, c);
         if (c == nch - 1) row_end(row);
     };
 
-    // software pipeline over this warp's chunk stream: chunk t + 1 loads while t computes
-    uint4 xa[kCh], xb[kCh];
-    load_chunk(xa, 0);
+    // software pipeline over this team's chunk stream: chunk t + 1 loads while t computes
     for (int t = 0; t < nchunks; t += 2) {
         load_chunk(xb, t + 1);
         step(xa, t);
@@ -445,7 +505,9 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
         load_chunk(xa, t + 2);
         step(xb, t + 1);
     }
-    if (lane == 0) ptx::bulk_wait_all();
+    mark(5);
+    if (tt == 0) ptx::bulk_wait_all();
+    mark(6);
     if (p.sat != nullptr) {
         sat = warp_sum(sat);
         if (lane == 0 && sat) atomicAdd(p.sat, sat);
@@ -463,14 +525,17 @@ void tier1_tables(const double* s, int64_t k, double act_scale, double t, double
 }
 
 bool flatten16(const FlattenArgs& a, cudaStream_t st) {
-    if (a.cj == nullptr || a.pj == nullptr || a.wsrc16 == nullptr || a.amax != nullptr)
+    if (a.cj == nullptr || a.pj == nullptr || a.wsrc16 == nullptr || a.hotg == nullptr ||
+        a.amax != nullptr)
         return false;
     if (a.x_dtype != FQG_BF16 && a.x_dtype != FQG_F16) return false;
-    if (a.k % 8 != 0 || a.k >= (1 << 24) || a.ldx % 8 != 0 || a.nhot > 32 * kHotRegs ||
+    if (a.k % 8 != 0 || a.k >= (1 << 24) || a.ldx % 8 != 0 || a.nhot > kMaxHot ||
         reinterpret_cast<uintptr_t>(a.x) % 16 != 0)
         return false;
     if (reinterpret_cast<uintptr_t>(a.q) % 16 != 0 || a.ldq % 16 != 0) return false;
-    const K1Smem w = k1_smem(static_cast<int>(a.k), static_cast<int>(a.kp), a.pack4);
+    constexpr int TW = 32;  // threads per row team
+    const K1Smem w = k1_smem(static_cast<int>(a.k), static_cast<int>(a.kp), static_cast<int>(a.c1),
+                             a.pack4, kWarps * 32 / TW);
     if (w.total > 220 * 1024) return false;
     K16Params p{};
     p.x = a.x;
@@ -481,8 +546,12 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     p.c1 = static_cast<int>(a.c1);
     p.ldf = w.ldf;
     p.nhot = static_cast<int>(a.nhot);
-    p.s_cj = w.cj, p.s_pj = w.pj, p.per_warp0 = w.per_warp0;
-    p.fl = w.fl, p.pk = w.pk, p.queue = w.queue, p.runs = w.runs, p.per_warp = w.per_warp;
+    p.s_cj = w.cj, p.s_pj = w.pj, p.s_wsrc = w.wsrc, p.s_hotm = w.hotm, p.per_team0 = w.per_team0;
+    p.s_hotg = w.hotg, p.s_tbar = w.tbar, p.hotg_bytes = w.hotg_bytes;
+    p.hotm = a.hotm;
+    p.hotg = a.hotg;
+    p.fl = w.fl, p.pk = w.pk, p.queue = w.queue, p.runs = w.runs, p.hotx = w.hotx;
+    p.per_team = w.per_team;
     p.cj = a.cj;
     p.pj = a.pj;
     p.hot = a.hot;
@@ -510,26 +579,48 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     p.ldq = a.ldq;
     p.sat = a.sat;
     p.rowsum = a.rowsum;
+    static const int dbg = [] {
+        const char* e = std::getenv("FQG_K1_DEBUG");
+        return e ? std::atoi(e) : 0;
+    }();
+    p.dbg = dbg;
+    if (dbg) {
+        static unsigned long long zeros[16] = {};
+        FQG_CUDA(cudaMemcpyToSymbol(g_k1dbg, zeros, sizeof(zeros)));
+    }
     auto run = [&](auto kern) {
         FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(w.total)));
         int occ = 0;
         FQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarps * 32, w.total));
-        const int64_t ctas_needed = (a.m + kWarps - 1) / kWarps;
+        constexpr int teams = kWarps * 32 / TW;
+        const int64_t ctas_needed = (a.m + teams - 1) / teams;
         const int grid = static_cast<int>(
             std::max<int64_t>(1, std::min<int64_t>(ctas_needed, std::max(1, occ) * a.num_sms)));
         kern<<<grid, kWarps * 32, w.total, st>>>(p);
         FQG_CUDA(cudaGetLastError());
+        if (dbg) {
+            unsigned long long h[16];
+            FQG_CUDA(cudaDeviceSynchronize());
+            FQG_CUDA(cudaMemcpyFromSymbol(h, g_k1dbg, sizeof(h)));
+            const double nt = static_cast<double>(grid) * (kWarps * 32 / 32);
+            std::fprintf(stderr,
+                         "[fqg k1] avg cycles since start per team: staged %.0f, row_begin done "
+                         "%.0f, tier1 done %.0f, tier2 done %.0f, runs done %.0f, copies done %.0f, "
+                         "loop end %.0f, stores done %.0f (grid %d)\n",
+                         h[0] / nt, h[7] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt,
+                         h[5] / nt, h[6] / nt, grid);
+        }
     };
     const bool f16 = a.x_dtype == FQG_F16;
     if (f16 && a.pack4)
-        run(k_flatten16<true, true>);
+        run(k_flatten16<true, true, TW>);
     else if (f16)
-        run(k_flatten16<true, false>);
+        run(k_flatten16<true, false, TW>);
     else if (a.pack4)
-        run(k_flatten16<false, true>);
+        run(k_flatten16<false, true, TW>);
     else
-        run(k_flatten16<false, false>);
+        run(k_flatten16<false, false, TW>);
     return true;
 }
 

@@ -34,6 +34,8 @@ struct FlattenArgs {
     const float* cj = nullptr;
     const uint16_t* pj = nullptr;
     const int32_t* hot = nullptr;  // channels always taking the exact path (pj = 0xFFFF)
+    const int32_t* hotm = nullptr; // [nhot] x {j, capacity, ext_offset, RN32(1/s_j) bits}
+    const int32_t* hotg = nullptr; // [k / 8] hot mask of the group | first hot index << 8
     int64_t nhot = 0;
     const int32_t* wsrc16 = nullptr;  // wsrc with padding (-1) mapped to column kp (a zero byte)
     double act_scale = 0.0;          // static s_x (host copy)

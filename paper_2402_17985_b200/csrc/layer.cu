@@ -45,7 +45,7 @@ struct fqg_layer_s {
     int64_t n_ext2 = 0;  // channels with >= 2 plan_x extension slots
     fqg::DevBuf d_s, d_rs, d_rs32, d_cap, d_off, d_wsrc, d_amap, d_wq, d_scale;
     // K1 16-bit certificates (flatten16.cu), static scale only: [0] bf16, [1] f16
-    fqg::DevBuf d_cj[2], d_pj[2], d_hot, d_wsrc16;
+    fqg::DevBuf d_cj[2], d_pj[2], d_hot, d_hotm, d_hotg, d_wsrc16;
     int64_t nhot = 0;
 };
 
@@ -222,6 +222,25 @@ fqg_layer_s* create(const fqg_layer_desc& d) {
             }
             L->nhot = static_cast<int64_t>(hot.size());
             upload(L->d_hot, hot);
+            // K1 tables for the hot channels: {j, capacity, ext_offset, RN32(1/s_j)}
+            // and, per group of 8 channels, hot mask | index of its first hot channel << 8.
+            std::vector<int32_t> hotm(4 * hot.size());
+            std::vector<int32_t> hotg(static_cast<size_t>((d.k / 8 + 3) / 4 * 4), 0);  // 16-byte multiple
+            for (size_t h = 0; h < hot.size(); ++h) {
+                const int32_t j = hot[h];
+                float r32 = rs32[j];
+                int32_t rbits;
+                std::memcpy(&rbits, &r32, 4);
+                hotm[4 * h] = j;
+                hotm[4 * h + 1] = g.cap_x[j];
+                hotm[4 * h + 2] = g.off_x[j];
+                hotm[4 * h + 3] = rbits;
+                int32_t& e = hotg[j / 8];
+                if ((e & 0xFF) == 0) e |= static_cast<int32_t>(h) << 8;
+                e |= 1 << (j % 8);
+            }
+            upload(L->d_hotm, hotm);
+            upload(L->d_hotg, hotg);
             std::vector<uint16_t> pj(static_cast<size_t>(d.k));
             for (int f = 0; f < 2 && !hot.empty(); ++f) {
                 FQG_CUDA(cudaMemcpy(pj.data(), L->d_pj[f].p, pj.size() * 2, cudaMemcpyDeviceToHost));
@@ -292,6 +311,8 @@ void quantize_acts(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, 
         a.cj = L->d_cj[f].as<float>();
         a.pj = L->d_pj[f].as<uint16_t>();
         a.hot = L->d_hot.as<int32_t>();
+        a.hotm = L->d_hotm.as<int32_t>();
+        a.hotg = L->d_hotg.as<int32_t>();
         a.nhot = L->nhot;
         a.wsrc16 = L->d_wsrc16.as<int32_t>();
         a.act_scale = L->act_scale;
