@@ -431,18 +431,23 @@ __device__ unsigned long long g_dbg2[296][8];  // pair packed path: see launch_p
 //   int8 operands: 2-SM TMA (completion counted on the leader's barrier);
 //   packed int4 operands: 1-SM TMA into this CTA's raw ring, local unpack
 //   warps expand to int8 and signal the leader.
-template <int STAGES, bool APK, bool BPK>
+// NB = 256-column blocks of B per tile: NB = 1 -> 256 x 256 tiles with a
+// double-buffered accumulator; NB = 2 -> 256 x 512 tiles, two accumulators
+// filling TMEM (no double buffer): the A tile is read once per two MMAs, so
+// L2 -> SMEM bytes per MAC drop by a quarter (the kernel is TMA-throughput bound).
+template <int STAGES, bool APK, bool BPK, int NB = 1>
 struct PairLayout {
     static constexpr int BN = 256;
+    static constexpr int NACC = NB == 1 ? 2 : 1;  // accumulator buffers
     static constexpr bool packed = APK || BPK;
     static constexpr int a_raw = APK ? BM * BK / 2 : BM * BK;       // own 128 rows of A
-    static constexpr int b_raw = BPK ? (BN / 2) * BK / 2 : (BN / 2) * BK;  // own half of B
+    static constexpr int b_raw = NB * (BPK ? (BN / 2) * BK / 2 : (BN / 2) * BK);  // own halves of B
     static constexpr int raw_stage = a_raw + b_raw;
     static constexpr int direct_bytes = (APK ? 0 : a_raw) + (BPK ? 0 : b_raw);
     static constexpr int packed_bytes = (APK ? a_raw : 0) + (BPK ? b_raw : 0);
-    static constexpr int USTAGES = packed ? 4 : 0;
+    static constexpr int USTAGES = packed ? (NB == 1 ? 4 : 2) : 0;
     static constexpr int a_unp = APK ? BM * BK : 0;
-    static constexpr int b_unp = BPK ? (BN / 2) * BK : 0;
+    static constexpr int b_unp = BPK ? NB * (BN / 2) * BK : 0;
     static constexpr int unp_stage = a_unp + b_unp;
     static constexpr int unp_off = STAGES * raw_stage;
     static constexpr int bar_off = unp_off + USTAGES * unp_stage;
@@ -450,22 +455,26 @@ struct PairLayout {
     static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
     static constexpr int unpack_warps = packed ? 8 : 0;
     static constexpr int threads = 256 + 32 * unpack_warps;
+    static constexpr int tmem_cols = NB == 1 ? 2 * BN : NB * BN;
     // Arrivals freeing a raw stage in each CTA: the leader's multicast MMA
     // commit when an operand is read straight from the raw stage, plus one per
     // local unpack warp that reads it.
     static constexpr int team_warps = unpack_warps / 2;  // alternate k-blocks, as in Layout
     static constexpr int raw_release = (direct_bytes > 0 ? 1 : 0) + (packed_bytes > 0 ? team_warps : 0);
+    static_assert(tmem_cols <= 512, "TMEM budget");
 };
 
-template <int STAGES, int OUT, int AF, int BF>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, AF != F8, BF != F8>::threads, 1)
+template <int STAGES, int OUT, int AF, int BF, int NB>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, AF != F8, BF != F8, NB>::threads, 1)
     k_gemm_i8_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
                    const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
                    int vec_ok, int dbg, const int32_t* __restrict__ rowsum, int sk,
                    int32_t* __restrict__ ws, int* __restrict__ ws_flag) {
     constexpr bool APK = AF != F8, BPK = BF != F8;
-    using L = PairLayout<STAGES, APK, BPK>;
+    using L = PairLayout<STAGES, APK, BPK, NB>;
+    constexpr int NACC = L::NACC;
+    constexpr int TN = NB * L::BN;  // tile columns
     const long long t_start = clock64();
     unsigned long long gstart = 0;
     if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gstart));
@@ -487,7 +496,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
     const int num_m = (m + 2 * BM - 1) / (2 * BM);
-    const int num_n = (n + BN - 1) / BN;
+    const int num_n = (n + TN - 1) / TN;
     const int num_tiles = num_m * num_n;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     // Work of this cluster as segments (tile, kb0, kb1). Data-parallel: whole
@@ -531,7 +540,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         ptx::fence_barrier_init();
     }
     if (warp == 1) {
-        ptx::tmem_alloc_pair(tmem_holder, 2 * BN);
+        ptx::tmem_alloc_pair(tmem_holder, L::tmem_cols);
         ptx::tmem_relinquish_pair();
     }
     ptx::tc_fence_before();
@@ -547,7 +556,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         for_each_seg([&](int tile, int kb0, int kb1) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const int a_row = m_blk * 2 * BM + rank * BM;
-            const int b_row = n_blk * BN + rank * (BN / 2);
+            const int b_row = n_blk * TN + rank * (BN / 2);  // + nb * BN per block
             for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
                 uint8_t* sa = smem + stage * L::raw_stage;
@@ -562,10 +571,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                     ptx::tma_load_2d_hint(sa, &tmA, &full_unp[stage], kb * BK / 2, a_row, keep);
                 else
                     ptx::tma_load_2d_2sm(sa, &tmA, lead_full, kb * BK, a_row, keep);
-                if constexpr (BPK)
-                    ptx::tma_load_2d_hint(sb, &tmB, &full_unp[stage], kb * BK / 2, b_row, keep);
-                else
-                    ptx::tma_load_2d_2sm(sb, &tmB, lead_full, kb * BK, b_row, keep);
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) {
+                    if constexpr (BPK)
+                        ptx::tma_load_2d_hint(sb + nb * (L::b_raw / NB), &tmB, &full_unp[stage],
+                                              kb * BK / 2, b_row + nb * BN, keep);
+                    else
+                        ptx::tma_load_2d_2sm(sb + nb * (L::b_raw / NB), &tmB, lead_full, kb * BK,
+                                             b_row + nb * BN, keep);
+                }
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -583,8 +597,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
         long long nkb_done = 0;
         for_each_seg([&](int, int kb0, int kb1) {
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
+            const int acc = it % NACC;
+            const uint32_t acc_phase = (it / NACC) & 1;
             FQG_TWAIT(2, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
             ptx::tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
@@ -598,9 +612,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                 const uint32_t b_addr = BPK ? unp + L::a_unp : raw + L::a_raw;
 #pragma unroll
                 for (int k = 0; k < BK / UK; ++k) {
-                    ptx::mma_i8_pair(d_tmem, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
-                                     ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
-                                     (kb != kb0 || k != 0) ? 1u : 0u);
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb)
+                        ptx::mma_i8_pair(d_tmem + nb * BN, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
+                                         ptx::smem_desc_sw128_kmajor(b_addr + nb * ((BN / 2) * BK) + k * UK),
+                                         idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                 }
                 if constexpr (L::direct_bytes > 0) ptx::mma_commit_pair(&empty[stage], 0x3);
                 if constexpr (L::packed) {
@@ -634,8 +650,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         int it = 0;
         for_each_seg([&](int tile, int kb0, int kb1) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
+            const int acc = it % NACC;
+            const uint32_t acc_phase = (it / NACC) & 1;
             const bool tail = kb0 > 0;        // partial sums -> ws[cid]
             const bool head = kb1 < num_kb;   // add ws[cid + 1] (its tail partial)
             ptx::mbar_wait(&tfull[acc], acc_phase);
@@ -661,7 +677,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                 __syncwarp();
             }
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
+            for (int c = 0; c < TN / 32; ++c) {
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
                 ptx::tmem_wait_ld();
@@ -681,7 +697,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                         r[4 * v] += pv.x, r[4 * v + 1] += pv.y, r[4 * v + 2] += pv.z, r[4 * v + 3] += pv.w;
                     }
                 }
-                const int col0 = n_blk * BN + c * 32;
+                const int col0 = n_blk * TN + c * 32;
                 if (row < m && col0 < n) {
                     const int ncols = min(32, n - col0);
                     store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
@@ -732,7 +748,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                 const uint8_t* raw = smem + stage * L::raw_stage;
                 uint8_t* unp = smem + L::unp_off + us * L::unp_stage;
                 if constexpr (APK) unpack_tile<AF>(raw, unp, BM, utid, nut);
-                if constexpr (BPK) unpack_tile<BF>(raw + L::a_raw, unp + L::a_unp, BN / 2, utid, nut);
+                if constexpr (BPK)
+                    unpack_tile<BF>(raw + L::a_raw, unp + L::a_unp, NB * (BN / 2), utid, nut);
                 if (d0) {
                     atomicAdd(&g_dbg2[blockIdx.x % 296][2], tw1 - tw0);
                     atomicAdd(&g_dbg2[blockIdx.x % 296][3], tw2 - tw1);
@@ -761,7 +778,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
     if (warp == 1) {
         __syncwarp();
         ptx::tc_fence_after();
-        ptx::tmem_dealloc_pair(tmem_base, 2 * BN);
+        ptx::tmem_dealloc_pair(tmem_base, L::tmem_cols);
     }
     if (dbg && threadIdx.x == 32) {
         unsigned long long gend;
@@ -1364,10 +1381,10 @@ void launch(const GemmArgs& g, cudaStream_t stream) {
     FQG_CUDA(cudaGetLastError());
 }
 
-template <int STAGES, int OUT, int AF, int BF>
+template <int STAGES, int OUT, int AF, int BF, int NB>
 void launch_pair(const GemmArgs& g, cudaStream_t stream) {
     constexpr bool APK = AF != F8, BPK = BF != F8;
-    using L = PairLayout<STAGES, APK, BPK>;
+    using L = PairLayout<STAGES, APK, BPK, NB>;
     static_assert(L::total <= 227 * 1024, "shared memory budget");
     CUtensorMap ta, tb;
     make_tmap_2d_u8(&ta, g.a, static_cast<uint64_t>(APK ? g.kp / 2 : g.kp),
@@ -1376,7 +1393,7 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
     make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(BPK ? g.kp / 2 : g.kp),
                     static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.ldb), BPK ? BK / 2 : BK,
                     L::BN / 2, BPK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
-    auto kern = k_gemm_i8_pair<STAGES, OUT, AF, BF>;
+    auto kern = k_gemm_i8_pair<STAGES, OUT, AF, BF, NB>;
     static bool attr_set = false;  // per instantiation
     if (!attr_set) {
         FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
@@ -1384,8 +1401,8 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
     }
     int dev = 0;
     FQG_CUDA(cudaGetDevice(&dev));
-    const int num_tiles =
-        static_cast<int>(((g.m + 2 * BM - 1) / (2 * BM)) * ((g.n + L::BN - 1) / L::BN));
+    const int num_tiles = static_cast<int>(((g.m + 2 * BM - 1) / (2 * BM)) *
+                                           ((g.n + NB * L::BN - 1) / (NB * L::BN)));
     const int clusters = std::max(1, std::min(num_tiles, num_sms(dev) / 2));
     const int esz = dtype_size(g.y_dtype);
     const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
@@ -1409,7 +1426,7 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
         return e ? std::atoi(e) : 0;
     }();
     const int64_t units = static_cast<int64_t>(num_tiles) * num_kb;
-    const bool sk = sk_env != 0 && num_tiles > clusters && num_tiles % clusters != 0 &&
+    const bool sk = NB == 1 && sk_env != 0 && num_tiles > clusters && num_tiles % clusters != 0 &&
                     units / clusters >= num_kb;
     int32_t* ws = nullptr;
     int* ws_flag = nullptr;
@@ -1472,13 +1489,30 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
 
 template <int AF, int BF>
 void dispatch_pair(const GemmArgs& g, cudaStream_t s) {
+    // 256 x 512 tiles (NB = 2) when N is wide enough; FQG_GEMM_NB overrides.
+    static const int nb_env = [] {
+        const char* e = std::getenv("FQG_GEMM_NB");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int nb = nb_env ? nb_env : (g.n >= 512 ? 2 : 1);
+    if (nb == 2) {
+        constexpr int ST = 4;
+        switch (g.y_dtype) {
+            case FQG_I32: return launch_pair<ST, FQG_I32, AF, BF, 2>(g, s);
+            case FQG_F64: return launch_pair<ST, FQG_F64, AF, BF, 2>(g, s);
+            case FQG_F32: return launch_pair<ST, FQG_F32, AF, BF, 2>(g, s);
+            case FQG_F16: return launch_pair<ST, FQG_F16, AF, BF, 2>(g, s);
+            case FQG_BF16: return launch_pair<ST, FQG_BF16, AF, BF, 2>(g, s);
+            default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
+        }
+    }
     constexpr int ST = 6;
     switch (g.y_dtype) {
-        case FQG_I32: return launch_pair<ST, FQG_I32, AF, BF>(g, s);
-        case FQG_F64: return launch_pair<ST, FQG_F64, AF, BF>(g, s);
-        case FQG_F32: return launch_pair<ST, FQG_F32, AF, BF>(g, s);
-        case FQG_F16: return launch_pair<ST, FQG_F16, AF, BF>(g, s);
-        case FQG_BF16: return launch_pair<ST, FQG_BF16, AF, BF>(g, s);
+        case FQG_I32: return launch_pair<ST, FQG_I32, AF, BF, 1>(g, s);
+        case FQG_F64: return launch_pair<ST, FQG_F64, AF, BF, 1>(g, s);
+        case FQG_F32: return launch_pair<ST, FQG_F32, AF, BF, 1>(g, s);
+        case FQG_F16: return launch_pair<ST, FQG_F16, AF, BF, 1>(g, s);
+        case FQG_BF16: return launch_pair<ST, FQG_BF16, AF, BF, 1>(g, s);
         default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
     }
 }
