@@ -323,7 +323,7 @@ def main():
         "breakdown_ms": {"flatten_quant_K1": t_k1, "gemm_K4": t_k4, "all_gather": t_ag},
         "roofline": {"bound": "tensor", "achieved": gemm_tops, "peak": int8_peak,
                      "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
-                     "kernel": "k_gemm_i8 (tcgen05.mma kind::i8)",
+                     "kernel": "k_gemm_i8_pair (tcgen05.mma.cta_group::2.kind::i8, 256x512 tiles)",
                      "peak_basis": f"tcgen05 kind::i8 MMA peak, {i8_src}; frac vs spec 4.5 "
                                    f"POPS: {gemm_tops / SPEC_INT8_TOPS:.3f}; vs 2 x bf16 "
                                    f"measured ({peak_src}): {gemm_tops / (2 * bf16_tf):.3f}",

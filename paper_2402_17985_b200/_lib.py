@@ -10,7 +10,7 @@ import os
 import subprocess
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libfqg.so")
+LIB_PATH = os.environ.get("FQG_LIB", os.path.join(PKG, "libfqg.so"))  # override: A/B builds
 CSRC = os.path.join(PKG, "csrc")
 
 # fqg_dtype

@@ -499,25 +499,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
     const int num_n = (n + TN - 1) / TN;
     const int num_tiles = num_m * num_n;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    // Work of this cluster as segments (tile, kb0, kb1). Data-parallel: whole
-    // tiles round robin. Stream-K (sk): the tile x k-block units are cut into
-    // ncl equal contiguous ranges (each >= one tile, so a tile is split at
-    // most two ways): a range that starts inside a tile leaves its partial
-    // INT32 sums in ws[cid] (flag += 8 warps); the cluster that owns the tile's
-    // head adds ws[cid + 1] in its epilogue (integer sums: exact, order-free).
+    // Work of this cluster as segments (tile, kb0, kb1, wslot, fslot, nf).
+    //  sk == 0: data-parallel, whole tiles round robin.
+    //  sk == 1: stream-K: the tile x k-block units are cut into ncl equal
+    //    contiguous ranges (each >= one tile, so a tile is split at most two
+    //    ways): a range that starts inside a tile leaves its partial INT32 sums
+    //    in ws[cid] (flag += 8 warps); the owner of the tile's head adds
+    //    ws[cid + 1] in its epilogue.
+    //  sk >= 2: split-K by sk (small M): unit u = cid is split s = u % sk of
+    //    tile u / sk; every split writes its raw INT32 partial to the full-size
+    //    plane ws[s][M][N] (wslot = -2 - s) and k_splitk_reduce sums the planes
+    //    and runs the epilogue.
+    // Integer partial sums: exact and order-free.
+    // Split modes only exist in the NB = 1 instantiation (small-M and ragged
+    // tile counts); the 256 x 512 kernel keeps the plain data-parallel loop.
+    constexpr bool SPLITS = NB == 1;
     auto for_each_seg = [&](auto&& f) {
-        if (sk) {
+        if (!SPLITS || sk == 0) {
+            for (int tile = cid; tile < num_tiles; tile += ncl) f(tile, 0, num_kb, -1, 0, 0);
+        } else if (sk == 1) {
             const int64_t total = static_cast<int64_t>(num_tiles) * num_kb;
             const int u0 = static_cast<int>(total * cid / ncl);
             const int u1 = static_cast<int>(total * (cid + 1) / ncl);
             for (int u = u0; u < u1;) {
                 const int tile = u / num_kb, kb0 = u % num_kb;
                 const int kb1 = min(num_kb, kb0 + (u1 - u));
-                f(tile, kb0, kb1);
+                f(tile, kb0, kb1, kb0 > 0 ? cid : -1, cid + 1, kb1 < num_kb ? 1 : 0);
                 u += kb1 - kb0;
             }
+        } else if (sk >= 2) {
+            if (cid < num_tiles * sk) {
+                const int tile = cid / sk, sp = cid % sk;
+                const int kb0 = sp * num_kb / sk, kb1 = (sp + 1) * num_kb / sk;
+                f(tile, kb0, kb1, -2 - sp, 0, 0);
+            }
         } else {
-            for (int tile = cid; tile < num_tiles; tile += ncl) f(tile, 0, num_kb);
+            for (int tile = cid; tile < num_tiles; tile += ncl) f(tile, 0, num_kb, -1, 0, 0);
         }
     };
 
@@ -553,7 +570,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         const uint64_t keep = ptx::policy_evict_last();
         int stage = 0;
         uint32_t phase = 0;
-        for_each_seg([&](int tile, int kb0, int kb1) {
+        for_each_seg([&](int tile, int kb0, int kb1, int, int, int) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const int a_row = m_blk * 2 * BM + rank * BM;
             const int b_row = n_blk * TN + rank * (BN / 2);  // + nb * BN per block
@@ -596,7 +613,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         unsigned long long g0;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
         long long nkb_done = 0;
-        for_each_seg([&](int, int kb0, int kb1) {
+        for_each_seg([&](int, int kb0, int kb1, int, int, int) {
             const int acc = it % NACC;
             const uint32_t acc_phase = (it / NACC) & 1;
             FQG_TWAIT(2, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
@@ -648,12 +665,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         const int ew = warp - 4;
         const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
         int it = 0;
-        for_each_seg([&](int tile, int kb0, int kb1) {
+        for_each_seg([&](int tile, int, int, int wslot, int fslot, int nf) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const int acc = it % NACC;
             const uint32_t acc_phase = (it / NACC) & 1;
-            const bool tail = kb0 > 0;        // partial sums -> ws[cid]
-            const bool head = kb1 < num_kb;   // add ws[cid + 1] (its tail partial)
+            const bool tail = SPLITS && wslot >= 0;    // partial sums -> ws[wslot]
+            const bool head = SPLITS && nf > 0;        // add ws[fslot .. fslot + nf)
+            const bool plane = SPLITS && wslot <= -2;  // split-K: raw partial -> plane -2 - wslot
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             unsigned long long ge0 = 0;
@@ -665,10 +683,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
             if (head) {
                 if (lane == 0) {
                     const long long tw0 = clock64();
-                    int v;
-                    do {
-                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ws_flag + cid + 1));
-                    } while (v < 8);
+                    for (int f = 0; f < nf; ++f) {
+                        int v;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];"
+                                         : "=r"(v)
+                                         : "l"(ws_flag + fslot + f));
+                        } while (v < 8);
+                    }
                     if (dbg && ew == 0) {
                         atomicAdd(&g_dbg2[blockIdx.x % 296][6], clock64() - tw0);
                         atomicAdd(&g_dbg2[blockIdx.x % 296][7], clock64() - t_start);
@@ -681,16 +703,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
                 ptx::tmem_wait_ld();
+                if (plane) {
+                    const int col0 = n_blk * TN + c * 32;
+                    if (row < m && col0 < n) {
+                        int32_t* dst = ws + (static_cast<int64_t>(-2 - wslot) * m + row) * n + col0;
+                        if (col0 + 32 <= n && (n & 3) == 0) {
+#pragma unroll
+                            for (int v = 0; v < 8; ++v)
+                                reinterpret_cast<int4*>(dst)[v] =
+                                    make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (col0 + e < n) dst[e] = static_cast<int32_t>(r[e]);
+                        }
+                    }
+                    continue;
+                }
                 if (tail) {
-                    int4* wp = reinterpret_cast<int4*>(ws + (static_cast<int64_t>(cid) * 256 + rloc) * 256 + c * 32);
+                    int4* wp = reinterpret_cast<int4*>(
+                        ws + (static_cast<int64_t>(wslot) * 256 + rloc) * TN + c * 32);
 #pragma unroll
                     for (int v = 0; v < 8; ++v)
                         wp[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
                     continue;
                 }
-                if (head) {
+                for (int f = 0; head && f < nf; ++f) {
                     const int4* wp = reinterpret_cast<const int4*>(
-                        ws + (static_cast<int64_t>(cid + 1) * 256 + rloc) * 256 + c * 32);
+                        ws + (static_cast<int64_t>(fslot + f) * 256 + rloc) * TN + c * 32);
 #pragma unroll
                     for (int v = 0; v < 8; ++v) {
                         const int4 pv = __ldcg(wp + v);
@@ -710,7 +750,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
             if (tail) {  // publish the partial: release at gpu scope, one arrival per warp
                 __threadfence();
                 __syncwarp();
-                if (lane == 0) atomicAdd(ws_flag + cid, 1);
+                if (lane == 0) atomicAdd(ws_flag + wslot, 1);
             }
             if (dbg && lane == 0 && ew == 0) {
                 unsigned long long ge1;
@@ -726,7 +766,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
         int stage = 0, us = 0, step = 0;
         uint32_t phase = 0, uphase = 0;
-        for_each_seg([&](int, int kb0, int kb1) {
+        for_each_seg([&](int, int kb0, int kb1, int, int, int) {
             for (int kb = kb0; kb < kb1; ++kb, ++step) {
                 if ((step & 1) != team) {
                     if (++us == U) {
@@ -1334,6 +1374,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
     }
 }
 
+// Split-K epilogue: y = epi(sum of the split planes), quantize.cpp:190-198
+// (+ the biased-int4 row-sum correction and the optional bias).
+template <int OUT>
+__global__ void __launch_bounds__(256)
+    k_splitk_reduce(const int32_t* __restrict__ ws, int splits, int m, int n, void* __restrict__ y,
+                    int64_t ldy, const double* __restrict__ scale, const void* __restrict__ bias,
+                    int bias_dt, const int32_t* __restrict__ rowsum) {
+    const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
+    const int64_t total = static_cast<int64_t>(m) * n;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        int32_t acc = 0;
+        for (int sp = 0; sp < splits; ++sp) acc += __ldcs(ws + sp * total + i);
+        const int row = static_cast<int>(i / n), col = static_cast<int>(i % n);
+        if (rowsum != nullptr) acc -= 8 * rowsum[row];
+        const double b = bias ? load_bias(bias, bias_dt, col) : 0.0;
+        store_one<OUT>(y, static_cast<int64_t>(row) * ldy + col, acc, s, b);
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -1426,20 +1486,41 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
         return e ? std::atoi(e) : 0;
     }();
     const int64_t units = static_cast<int64_t>(num_tiles) * num_kb;
-    const bool sk = NB == 1 && sk_env != 0 && num_tiles > clusters && num_tiles % clusters != 0 &&
-                    units / clusters >= num_kb;
+    int sk = (NB == 1 && sk_env != 0 && num_tiles > clusters && num_tiles % clusters != 0 &&
+              units / clusters >= num_kb)
+                 ? 1
+                 : 0;
+    // Split-K for small M: fewer than half the clusters would have a tile.
+    const int max_clusters = std::max(1, num_sms(dev) / 2);
+    if (sk == 0 && 2 * num_tiles <= max_clusters && num_kb >= 8) {
+        int splits = std::min({max_clusters / num_tiles, num_kb / 4, 8});
+        if (splits >= 2) sk = splits;
+    }
+    const int nclusters = sk >= 2 ? num_tiles * sk : clusters;
     int32_t* ws = nullptr;
     int* ws_flag = nullptr;
-    if (sk) {
-        const size_t wbytes = static_cast<size_t>(clusters + 1) * 256 * 256 * 4;
-        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes + (clusters + 1) * 4, stream));
+    if (sk == 1) {
+        const int slots = nclusters + 1;
+        const size_t wbytes = static_cast<size_t>(slots) * 256 * (NB * L::BN) * 4;
+        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes + slots * 4, stream));
         ws_flag = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + wbytes);
-        FQG_CUDA(cudaMemsetAsync(ws_flag, 0, (clusters + 1) * 4, stream));
+        FQG_CUDA(cudaMemsetAsync(ws_flag, 0, slots * 4, stream));
+    } else if (sk >= 2) {
+        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws),
+                                 static_cast<size_t>(sk) * g.m * g.n * 4, stream));
     }
-    kern<<<2 * clusters, L::threads, L::total, stream>>>(
+    kern<<<2 * nclusters, L::threads, L::total, stream>>>(
         ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb, g.scale, g.bias,
-        g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk ? 1 : 0, ws, ws_flag);
-    const cudaError_t le = cudaGetLastError();
+        g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk, ws, ws_flag);
+    cudaError_t le = cudaGetLastError();
+    if (le == cudaSuccess && sk >= 2) {
+        const int64_t total = g.m * g.n;
+        const int rgrid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * num_sms(dev)));
+        k_splitk_reduce<OUT><<<rgrid, 256, 0, stream>>>(
+            ws, sk, static_cast<int>(g.m), static_cast<int>(g.n), g.y, g.ldy, g.scale, g.bias,
+            g.bias_dtype, BF == FU4 ? g.rowsum : nullptr);
+        le = cudaGetLastError();
+    }
     if (ws) cudaFreeAsync(ws, stream);
     FQG_CUDA(le);
     if (dbg) {
@@ -1447,7 +1528,7 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
         FQG_CUDA(cudaDeviceSynchronize());
         FQG_CUDA(cudaMemcpyFromSymbol(h, g_dbg, sizeof(h)));
         double acc[8] = {0};
-        const int nc = 2 * clusters;
+        const int nc = 2 * nclusters;
         for (int c = 0; c < nc; ++c)
             for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(h[c][i]) / nc;
         // leader-only slots are averaged over both CTAs of a pair: x2
@@ -1470,6 +1551,13 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
                      "[fqg gemm pair] CTA start spread %.1f us, end spread %.1f..%.1f us after "
                      "first start; per-leader mma loop %.1f us avg\n",
                      (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, (e1 - s0) * 1e-3, acc[4] * 2e-3);
+        for (int c = 0; c < nc; ++c)
+            if (h[c][3] - s0 > (e1 - s0) * 0.8 || (c >= 112 && c < 128))
+                std::fprintf(stderr,
+                             "[fqg gemm pair]   slow CTA %d (cluster %d, rank %d): start %.1f end %.1f us; "
+                             "mma loop %llu ns; epi %llu ns over %llu tiles\n",
+                             c, c / 2, c % 2, (h[c][0] - s0) * 1e-3, (h[c][3] - s0) * 1e-3, h[c][4],
+                             h[c][1], h[c][2]);
         std::fprintf(stderr, "[fqg gemm pair] epilogue per tile (warp 0 of 4): %.2f us\n",
                      acc[2] > 0 ? acc[1] / acc[2] * 1e-3 : 0.0);
         unsigned long long h2[296][8];
@@ -1494,7 +1582,10 @@ void dispatch_pair(const GemmArgs& g, cudaStream_t s) {
         const char* e = std::getenv("FQG_GEMM_NB");
         return e ? std::atoi(e) : 0;
     }();
-    const int nb = nb_env ? nb_env : (g.n >= 512 ? 2 : 1);
+    // NB = 2 needs enough 256 x 512 tiles to fill the 74 CTA pairs; otherwise
+    // 256 x 256 tiles (plus split-K when even those are few).
+    const int64_t t2 = ((g.m + 255) / 256) * ((g.n + 511) / 512);
+    const int nb = nb_env ? nb_env : (g.n >= 512 && t2 >= 48 ? 2 : 1);
     if (nb == 2) {
         constexpr int ST = 4;
         switch (g.y_dtype) {

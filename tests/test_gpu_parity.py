@@ -238,11 +238,12 @@ def test_full_size_row_subset(port, fq, bits, a_fmt, b_fmt):
     fp16_close(y16[rows], y_ref)
 
 
-@pytest.mark.parametrize("m,n,kp", [(512, 10240, 1024), (2048, 4096, 512), (300, 8960, 2048)])
+@pytest.mark.parametrize("m,n,kp", [(512, 10240, 1024), (2048, 4096, 512), (300, 8960, 2048),
+                                    (256, 4096, 7296), (200, 1024, 4096)])
 def test_gemm_stream_k_shapes(fq, m, n, kp):
-    """Shapes whose 256x256 tile count leaves a partial last round on 74 CTA
-    pairs: the stream-K split (two clusters per tile, INT32 partials through a
-    workspace) must give the exact integer product."""
+    """Tile counts that leave CTA pairs idle: split-K (small M, INT32 partials
+    of 2..8 clusters per tile through a workspace) and the optional stream-K
+    must give the exact integer product."""
     import torch
 
     from paper_2402_17985_b200 import _lib
