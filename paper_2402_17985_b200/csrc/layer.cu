@@ -470,34 +470,66 @@ int fqg_layer_gemm(fqg_layer_t L, const void* q, int64_t m, void* y, int y_dtype
     return fqg_layer_gemm_ex(L, q, nullptr, m, y, y_dtype, ldy, bias, bias_dtype, stream);
 }
 
+// The drop-in host call, pipelined: M is cut into row chunks that alternate
+// between two streams, so the host->device copy of chunk c + 1, the kernels of
+// chunk c and the device->host copy of chunk c - 1 overlap (PCIe is full
+// duplex). Rows are independent under the static scale, so chunking is exact.
 int fqg_layer_run_host(fqg_layer_t L, const double* x_host, int64_t m, double* y_host,
                        int64_t* saturation) {
     return guard([&] {
         require(L != nullptr && x_host && y_host, "run_layer: null argument");
         require(m >= 1, "run_layer: empty input");
         DeviceGuard dg(L->device);
-        cudaStream_t st = cudaStreamPerThread;
+        static thread_local cudaStream_t streams[64][2] = {};
+        cudaStream_t* ss = streams[L->device & 63];
+        for (int i = 0; i < 2; ++i)
+            if (ss[i] == nullptr) FQG_CUDA(cudaStreamCreateWithFlags(&ss[i], cudaStreamNonBlocking));
+        cudaStream_t st = ss[0];
         void *dx = nullptr, *dy = nullptr;
         unsigned long long* dsat = nullptr;
         const size_t xb = static_cast<size_t>(m * L->k) * 8, yb = static_cast<size_t>(m * L->n) * 8;
         FQG_CUDA(cudaMallocAsync(&dx, xb, st));
         FQG_CUDA(cudaMallocAsync(&dy, yb, st));
         FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dsat), 8, st));
+        cudaEvent_t ev[2];
+        FQG_CUDA(cudaEventCreateWithFlags(&ev[0], cudaEventDisableTiming));
+        FQG_CUDA(cudaEventCreateWithFlags(&ev[1], cudaEventDisableTiming));
         struct Free {
             void *a, *b, *c;
-            cudaStream_t s;
+            cudaStream_t s0, s1;
+            cudaEvent_t e0, e1;
             ~Free() {
-                cudaFreeAsync(a, s);
-                cudaFreeAsync(b, s);
-                cudaFreeAsync(c, s);
-                cudaStreamSynchronize(s);
+                cudaEventRecord(e1, s1);  // stream 1's work done before the frees
+                cudaStreamWaitEvent(s0, e1, 0);
+                cudaFreeAsync(a, s0);
+                cudaFreeAsync(b, s0);
+                cudaFreeAsync(c, s0);
+                cudaStreamSynchronize(s0);
+                cudaEventDestroy(e0);
+                cudaEventDestroy(e1);
             }
-        } fr{dx, dy, dsat, st};
+        } fr{dx, dy, dsat, ss[0], ss[1], ev[0], ev[1]};
         FQG_CUDA(cudaMemsetAsync(dsat, 0, 8, st));
-        FQG_CUDA(cudaMemcpyAsync(dx, x_host, xb, cudaMemcpyHostToDevice, st));
-        forward(L, dx, FQG_F64, m, dy, FQG_F64, L->n, nullptr, FQG_NONE, dsat, st);
+        FQG_CUDA(cudaEventRecord(ev[0], st));  // allocations + zeroed counter visible to stream 1
+        FQG_CUDA(cudaStreamWaitEvent(ss[1], ev[0], 0));
+        // ~8 chunks of >= 128 rows (a multiple of 32 keeps the GEMM tiles full)
+        const int64_t chunk = std::max<int64_t>(128, ((m + 7) / 8 + 31) / 32 * 32);
+        int ci = 0;
+        for (int64_t r0 = 0; r0 < m; r0 += chunk, ++ci) {
+            const int64_t mc = std::min(chunk, m - r0);
+            cudaStream_t s = ss[ci & 1];
+            const double* xs = x_host + r0 * L->k;
+            double* dxs = static_cast<double*>(dx) + r0 * L->k;
+            double* dys = static_cast<double*>(dy) + r0 * L->n;
+            FQG_CUDA(cudaMemcpyAsync(dxs, xs, static_cast<size_t>(mc * L->k) * 8,
+                                     cudaMemcpyHostToDevice, s));
+            forward(L, dxs, FQG_F64, mc, dys, FQG_F64, L->n, nullptr, FQG_NONE, dsat, s);
+            FQG_CUDA(cudaMemcpyAsync(y_host + r0 * L->n, dys, static_cast<size_t>(mc * L->n) * 8,
+                                     cudaMemcpyDeviceToHost, s));
+        }
+        FQG_CUDA(cudaEventRecord(ev[1], ss[1]));
+        FQG_CUDA(cudaStreamWaitEvent(st, ev[1], 0));
         unsigned long long sat = 0;
-        FQG_CUDA(cudaMemcpyAsync(y_host, dy, yb, cudaMemcpyDeviceToHost, st));
         FQG_CUDA(cudaMemcpyAsync(&sat, dsat, 8, cudaMemcpyDeviceToHost, st));
         FQG_CUDA(cudaStreamSynchronize(st));
         if (saturation) *saturation = static_cast<int64_t>(sat);
