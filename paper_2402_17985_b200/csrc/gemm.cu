@@ -721,19 +721,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                     continue;
                 }
                 if (tail) {
-                    int4* wp = reinterpret_cast<int4*>(
-                        ws + (static_cast<int64_t>(wslot) * 256 + rloc) * TN + c * 32);
+                    // slot layout [chunk][v][256 rows][4]: each store instruction of a warp
+                    // writes 512 contiguous bytes
+                    int4* wp = reinterpret_cast<int4*>(ws + static_cast<int64_t>(wslot) * 256 * TN) +
+                               c * 8 * 256 + rloc;
 #pragma unroll
                     for (int v = 0; v < 8; ++v)
-                        wp[v] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+                        wp[v * 256] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
                     continue;
                 }
                 for (int f = 0; head && f < nf; ++f) {
-                    const int4* wp = reinterpret_cast<const int4*>(
-                        ws + (static_cast<int64_t>(fslot + f) * 256 + rloc) * TN + c * 32);
+                    const int4* wp =
+                        reinterpret_cast<const int4*>(ws + static_cast<int64_t>(fslot + f) * 256 * TN) +
+                        c * 8 * 256 + rloc;
 #pragma unroll
                     for (int v = 0; v < 8; ++v) {
-                        const int4 pv = __ldcg(wp + v);
+                        const int4 pv = __ldcg(wp + v * 256);
                         r[4 * v] += pv.x, r[4 * v + 1] += pv.y, r[4 * v + 2] += pv.z, r[4 * v + 3] += pv.w;
                     }
                 }
