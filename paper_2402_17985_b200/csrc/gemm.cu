@@ -22,6 +22,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -204,6 +205,27 @@ __device__ __forceinline__ void store_row_chunk(void* y, int64_t base, uint32_t 
             const double b = bias ? load_bias(bias, bias_dt, col0 + c) : 0.0;
             store_one<OUT>(y, base + c, static_cast<int32_t>(r[c]), s, b);
         }
+    }
+}
+
+template <int OUT>
+struct OutT;
+template <> struct OutT<FQG_I32> { using T = int32_t; };
+template <> struct OutT<FQG_F64> { using T = double; };
+template <> struct OutT<FQG_F32> { using T = float; };
+template <> struct OutT<FQG_F16> { using T = __half; };
+template <> struct OutT<FQG_BF16> { using T = __nv_bfloat16; };
+
+template <int OUT>
+__device__ __forceinline__ typename OutT<OUT>::T convert_out(int32_t acc, double s, double b) {
+    if constexpr (OUT == FQG_I32) {
+        return acc;
+    } else {
+        const double v = static_cast<double>(acc) * s + b;  // quantize.cpp:196 (+ bias)
+        if constexpr (OUT == FQG_F64) return v;
+        if constexpr (OUT == FQG_F32) return static_cast<float>(v);
+        if constexpr (OUT == FQG_F16) return __double2half(v);
+        if constexpr (OUT == FQG_BF16) return __double2bfloat16(v);
     }
 }
 
@@ -435,7 +457,7 @@ __device__ unsigned long long g_dbg2[296][8];  // pair packed path: see launch_p
 // double-buffered accumulator; NB = 2 -> 256 x 512 tiles, two accumulators
 // filling TMEM (no double buffer): the A tile is read once per two MMAs, so
 // L2 -> SMEM bytes per MAC drop by a quarter (the kernel is TMA-throughput bound).
-template <int STAGES, bool APK, bool BPK, int NB = 1>
+template <int STAGES, bool APK, bool BPK, int NB = 1, int EPIB = 0>
 struct PairLayout {
     static constexpr int BN = 256;
     static constexpr int NACC = NB == 1 ? 2 : 1;  // accumulator buffers
@@ -450,7 +472,10 @@ struct PairLayout {
     static constexpr int b_unp = BPK ? NB * (BN / 2) * BK : 0;
     static constexpr int unp_stage = a_unp + b_unp;
     static constexpr int unp_off = STAGES * raw_stage;
-    static constexpr int bar_off = unp_off + USTAGES * unp_stage;
+    // epilogue staging: per epilogue warp 2 buffers of a 32 x 32 output block
+    // (the box of a TMA tensor store); EPIB = bytes of one block, 0 = direct stores
+    static constexpr int epi_off = unp_off + USTAGES * unp_stage;
+    static constexpr int bar_off = epi_off + 4 * 2 * EPIB;
     static constexpr int n_bars = 3 * STAGES + 2 * USTAGES + 4;
     static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
     static constexpr int unpack_warps = packed ? 8 : 0;
@@ -464,15 +489,27 @@ struct PairLayout {
     static_assert(tmem_cols <= 512, "TMEM budget");
 };
 
+// Staged TMA-store epilogue for 4-byte outputs (f32 at 2048x4096: 97 -> 71 us);
+// 2-byte outputs keep direct 16-byte stores (measured faster: 60 vs 66 us),
+// f64 keeps direct stores (the staging would not fit next to the rings).
+template <int OUT>
+constexpr int epi_block_bytes() {
+    return (OUT == FQG_F32 || OUT == FQG_I32) ? 32 * 32 * 4 : 0;
+}
+
 template <int STAGES, int OUT, int AF, int BF, int NB>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, AF != F8, BF != F8, NB>::threads, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
+    PairLayout<STAGES, AF != F8, BF != F8, NB, epi_block_bytes<OUT>()>::threads, 1)
     k_gemm_i8_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
                    const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
                    int vec_ok, int dbg, const int32_t* __restrict__ rowsum, int sk,
-                   int32_t* __restrict__ ws, int* __restrict__ ws_flag) {
+                   int32_t* __restrict__ ws, int* __restrict__ ws_flag,
+                   const __grid_constant__ CUtensorMap tmY, int tma_y) {
     constexpr bool APK = AF != F8, BPK = BF != F8;
-    using L = PairLayout<STAGES, APK, BPK, NB>;
+    constexpr int EPIB = epi_block_bytes<OUT>();
+    using L = PairLayout<STAGES, APK, BPK, NB, EPIB>;
+    using OT = typename OutT<OUT>::T;
     constexpr int NACC = L::NACC;
     constexpr int TN = NB * L::BN;  // tile columns
     const long long t_start = clock64();
@@ -664,7 +701,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
         // ---------------- epilogue (both CTAs: own 128 rows) ----------------
         const int ew = warp - 4;
         const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
-        int it = 0;
+        int it = 0, echunk = 0;
+        if (EPIB > 0 && tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
         for_each_seg([&](int tile, int, int, int wslot, int fslot, int nf) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const int acc = it % NACC;
@@ -675,7 +713,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             unsigned long long ge0 = 0;
-            if (dbg && lane == 0 && ew == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
+            if (dbg && lane == 0 && ew == 0) {
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
+                atomicAdd(&g_dbg2[blockIdx.x % 296][6], ge0 - gstart);  // tfull reached (ns)
+            }
             const int rloc = rank * BM + ew * 32 + lane;  // row within the 256-row tile
             const int row = m_blk * 2 * BM + rloc;
             const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
@@ -691,10 +732,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                                          : "l"(ws_flag + fslot + f));
                         } while (v < 8);
                     }
-                    if (dbg && ew == 0) {
-                        atomicAdd(&g_dbg2[blockIdx.x % 296][6], clock64() - tw0);
-                        atomicAdd(&g_dbg2[blockIdx.x % 296][7], clock64() - t_start);
-                    }
+                    (void)tw0;
                 }
                 __syncwarp();
             }
@@ -741,6 +779,39 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                     }
                 }
                 const int col0 = n_blk * TN + c * 32;
+                if constexpr (EPIB > 0) {
+                    if (tma_y) {  // convert, stage the 32 x 32 block, one TMA tensor store
+                        uint8_t* ep = smem + L::epi_off + (ew * 2 + (echunk & 1)) * EPIB;
+                        ++echunk;
+                        if (lane == 0) ptx::bulk_wait_read_allbut1();
+                        __syncwarp();
+                        constexpr int ESZ = static_cast<int>(sizeof(OT));
+                        uint32_t wv[32 * ESZ / 4];
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            const double bv =
+                                bias != nullptr ? load_bias(bias, bias_dt, min(col0 + e, n - 1)) : 0.0;
+                            const OT v = convert_out<OUT>(static_cast<int32_t>(r[e]) - corr, s, bv);
+                            if constexpr (ESZ == 4) {
+                                wv[e] = *reinterpret_cast<const uint32_t*>(&v);
+                            } else {
+                                const uint32_t h = *reinterpret_cast<const uint16_t*>(&v);
+                                wv[e >> 1] = (e & 1) ? (wv[e >> 1] | (h << 16)) : h;
+                            }
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(ep + lane * 32 * ESZ);
+#pragma unroll
+                        for (int v = 0; v < 8 * ESZ / 4; ++v)
+                            dst[v] = make_uint4(wv[4 * v], wv[4 * v + 1], wv[4 * v + 2], wv[4 * v + 3]);
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_2d(&tmY, ep, col0, m_blk * 2 * BM + rank * BM + ew * 32);
+                            ptx::bulk_commit();
+                        }
+                        continue;
+                    }
+                }
                 if (row < m && col0 < n) {
                     const int ncols = min(32, n - col0);
                     store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
@@ -760,9 +831,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(PairLayout<STAGES, A
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge1));
                 atomicAdd(&g_dbg[blockIdx.x % 296][1], ge1 - ge0);
                 atomicAdd(&g_dbg[blockIdx.x % 296][2], 1ull);
+                atomicAdd(&g_dbg2[blockIdx.x % 296][7], ge1 - gstart);  // epilogue done (ns)
             }
             ++it;
         });
+        if (EPIB > 0 && tma_y && lane == 0) ptx::bulk_wait_all();  // staged output stores
     } else if (L::packed && warp >= 8) {
         // ---------------- int4 -> int8 unpack warps (both CTAs) ----------------
         const int team = (warp - 8) / L::team_warps;
@@ -859,27 +932,6 @@ struct W4Layout {
     static constexpr uint32_t a_col0 = 2 * BN;
     static_assert(2 * BN + 32 * kW4AStages <= 512, "TMEM budget");
 };
-
-template <int OUT>
-struct OutT;
-template <> struct OutT<FQG_I32> { using T = int32_t; };
-template <> struct OutT<FQG_F64> { using T = double; };
-template <> struct OutT<FQG_F32> { using T = float; };
-template <> struct OutT<FQG_F16> { using T = __half; };
-template <> struct OutT<FQG_BF16> { using T = __nv_bfloat16; };
-
-template <int OUT>
-__device__ __forceinline__ typename OutT<OUT>::T convert_out(int32_t acc, double s, double b) {
-    if constexpr (OUT == FQG_I32) {
-        return acc;
-    } else {
-        const double v = static_cast<double>(acc) * s + b;  // quantize.cpp:196 (+ bias)
-        if constexpr (OUT == FQG_F64) return v;
-        if constexpr (OUT == FQG_F32) return static_cast<float>(v);
-        if constexpr (OUT == FQG_F16) return __double2half(v);
-        if constexpr (OUT == FQG_BF16) return __double2bfloat16(v);
-    }
-}
 
 template <int BN, int STAGES, int OUT>
 __global__ void __launch_bounds__(512, 1)
@@ -1447,7 +1499,7 @@ void launch(const GemmArgs& g, cudaStream_t stream) {
 template <int STAGES, int OUT, int AF, int BF, int NB>
 void launch_pair(const GemmArgs& g, cudaStream_t stream) {
     constexpr bool APK = AF != F8, BPK = BF != F8;
-    using L = PairLayout<STAGES, APK, BPK, NB>;
+    using L = PairLayout<STAGES, APK, BPK, NB, epi_block_bytes<OUT>()>;
     static_assert(L::total <= 227 * 1024, "shared memory budget");
     CUtensorMap ta, tb;
     make_tmap_2d_u8(&ta, g.a, static_cast<uint64_t>(APK ? g.kp / 2 : g.kp),
@@ -1512,9 +1564,26 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
         FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws),
                                  static_cast<size_t>(sk) * g.m * g.n * 4, stream));
     }
+    CUtensorMap ty;
+    std::memset(&ty, 0, sizeof(ty));
+    const bool tma_y = epi_block_bytes<OUT>() > 0 && vec && sk < 2;
+    if (tma_y) {
+        const CUtensorMapDataType dt =
+            esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(g.m)};
+        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.ldy * esz)};
+        const cuuint32_t box[2] = {32, 32};
+        const cuuint32_t estr[2] = {1, 1};
+        const CUresult r = encode_fn()(&ty, dt, 2, g.y, dims, strides, box, estr,
+                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                       CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS)
+            throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed (" + std::to_string(r) + ")");
+    }
     kern<<<2 * nclusters, L::threads, L::total, stream>>>(
         ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb, g.scale, g.bias,
-        g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk, ws, ws_flag);
+        g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk, ws, ws_flag, ty, tma_y ? 1 : 0);
     cudaError_t le = cudaGetLastError();
     if (le == cudaSuccess && sk >= 2) {
         const int64_t total = g.m * g.n;
@@ -1568,14 +1637,30 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
         double a2[8] = {0};
         for (int c = 0; c < nc; ++c)
             for (int i = 0; i < 8; ++i) a2[i] += static_cast<double>(h2[c][i]) / nc;
-        std::fprintf(stderr, "[fqg gemm pair] stream-K head: flag wait %.0f cyc, reached at %.0f cyc\n",
-                     a2[6], a2[7]);
+        std::fprintf(stderr, "[fqg gemm pair] epilogue: accumulator ready at %.1f us, done at %.1f us (avg per CTA, summed over its tiles)\n",
+                     a2[6] * 1e-3, a2[7] * 1e-3);
         std::fprintf(stderr,
                      "[fqg gemm pair] per CTA: mma wait ufull %.0f, wait full_mma %.0f | unpack "
                      "(thread 0): wait full_unp %.0f, wait uempty %.0f, work %.0f cyc over %.0f "
                      "k-blocks\n",
                      a2[0] * 2, a2[1] * 2, a2[2], a2[3], a2[4], a2[5]);
     }
+}
+
+// Largest raw-ring depth (<= maxst) that fits the shared-memory budget.
+template <bool APK, bool BPK, int NB, int EPIB>
+constexpr int fit_stages(int maxst) {
+    using L1 = PairLayout<1, APK, BPK, NB, EPIB>;
+    const int fixed = L1::USTAGES * L1::unp_stage + 4 * 2 * EPIB + 1024 + 64 * 8 + 16;
+    const int st = (227 * 1024 - fixed) / L1::raw_stage;
+    return st < maxst ? st : maxst;
+}
+
+template <int AF, int BF, int NB, int OUT>
+void launch_pair_fit(const GemmArgs& g, cudaStream_t s) {
+    constexpr int ST = fit_stages<AF != F8, BF != F8, NB, epi_block_bytes<OUT>()>(NB == 1 ? 6 : 4);
+    static_assert(ST >= 2, "pipeline depth");
+    launch_pair<ST, OUT, AF, BF, NB>(g, s);
 }
 
 template <int AF, int BF>
@@ -1589,26 +1674,19 @@ void dispatch_pair(const GemmArgs& g, cudaStream_t s) {
     // 256 x 256 tiles (plus split-K when even those are few).
     const int64_t t2 = ((g.m + 255) / 256) * ((g.n + 511) / 512);
     const int nb = nb_env ? nb_env : (g.n >= 512 && t2 >= 48 ? 2 : 1);
-    if (nb == 2) {
-        constexpr int ST = 4;
+    auto go = [&](auto nbc) {
+        constexpr int NB = decltype(nbc)::value;
         switch (g.y_dtype) {
-            case FQG_I32: return launch_pair<ST, FQG_I32, AF, BF, 2>(g, s);
-            case FQG_F64: return launch_pair<ST, FQG_F64, AF, BF, 2>(g, s);
-            case FQG_F32: return launch_pair<ST, FQG_F32, AF, BF, 2>(g, s);
-            case FQG_F16: return launch_pair<ST, FQG_F16, AF, BF, 2>(g, s);
-            case FQG_BF16: return launch_pair<ST, FQG_BF16, AF, BF, 2>(g, s);
+            case FQG_I32: return launch_pair_fit<AF, BF, NB, FQG_I32>(g, s);
+            case FQG_F64: return launch_pair_fit<AF, BF, NB, FQG_F64>(g, s);
+            case FQG_F32: return launch_pair_fit<AF, BF, NB, FQG_F32>(g, s);
+            case FQG_F16: return launch_pair_fit<AF, BF, NB, FQG_F16>(g, s);
+            case FQG_BF16: return launch_pair_fit<AF, BF, NB, FQG_BF16>(g, s);
             default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
         }
-    }
-    constexpr int ST = 6;
-    switch (g.y_dtype) {
-        case FQG_I32: return launch_pair<ST, FQG_I32, AF, BF, 1>(g, s);
-        case FQG_F64: return launch_pair<ST, FQG_F64, AF, BF, 1>(g, s);
-        case FQG_F32: return launch_pair<ST, FQG_F32, AF, BF, 1>(g, s);
-        case FQG_F16: return launch_pair<ST, FQG_F16, AF, BF, 1>(g, s);
-        case FQG_BF16: return launch_pair<ST, FQG_BF16, AF, BF, 1>(g, s);
-        default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
-    }
+    };
+    if (nb == 2) return go(std::integral_constant<int, 2>{});
+    return go(std::integral_constant<int, 1>{});
 }
 
 template <int BN, int AF, int BF>
