@@ -479,7 +479,11 @@ struct PairLayout {
     static constexpr int n_bars = 3 * STAGES + 2 * USTAGES + 4;
     static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
     static constexpr int unpack_warps = packed ? 8 : 0;
-    static constexpr int threads = 256 + 32 * unpack_warps;
+    // epilogue warp groups (4 warps each): NB = 2 drains its single accumulator
+    // after the main loop with the unpack warps (or 4 spare warps) joining in
+    // (4-byte outputs keep one group and the staged TMA-store epilogue instead)
+    static constexpr int epi_groups = (NB == 2 && EPIB != 32 * 32 * 4) ? (packed ? 3 : 2) : 1;
+    static constexpr int threads = 256 + 32 * (packed ? unpack_warps : (epi_groups - 1) * 4);
     static constexpr int tmem_cols = NB == 1 ? 2 * BN : NB * BN;
     // Arrivals freeing a raw stage in each CTA: the leader's multicast MMA
     // commit when an operand is read straight from the raw stage, plus one per
@@ -511,6 +515,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     using L = PairLayout<STAGES, APK, BPK, NB, EPIB>;
     using OT = typename OutT<OUT>::T;
     constexpr int NACC = L::NACC;
+    constexpr int NG = L::epi_groups;
     constexpr int TN = NB * L::BN;  // tile columns
     const long long t_start = clock64();
     unsigned long long gstart = 0;
@@ -589,7 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 8);
+            ptx::mbar_init(&tempty[a], 8 * NG);
         }
         ptx::fence_barrier_init();
     }
@@ -601,6 +606,149 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+
+    // ---------------- epilogue (both CTAs: own 128 rows) ----------------
+    // Lane quarter ew of TMEM; group grp of NG takes chunks grp, grp + NG, ...
+    // (with one accumulator, NB = 2, the unpack warps / spare warps join after
+    // the main loop so the exposed drain is split NG ways).
+    auto run_epilogue = [&](const int ew, const int grp) {
+        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
+        int it = 0, echunk = 0;
+        if (EPIB > 0 && tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
+        for_each_seg([&](int tile, int, int, int wslot, int fslot, int nf) {
+            const int m_blk = tile % num_m, n_blk = tile / num_m;
+            const int acc = it % NACC;
+            const uint32_t acc_phase = (it / NACC) & 1;
+            const bool tail = SPLITS && wslot >= 0;    // partial sums -> ws[wslot]
+            const bool head = SPLITS && nf > 0;        // add ws[fslot .. fslot + nf)
+            const bool plane = SPLITS && wslot <= -2;  // split-K: raw partial -> plane -2 - wslot
+            ptx::mbar_wait(&tfull[acc], acc_phase);
+            ptx::tc_fence_after();
+            unsigned long long ge0 = 0;
+            if (dbg && lane == 0 && ew == 0 && grp == 0) {
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
+                atomicAdd(&g_dbg2[blockIdx.x % 296][6], ge0 - gstart);  // tfull reached (ns)
+            }
+            const int rloc = rank * BM + ew * 32 + lane;  // row within the 256-row tile
+            const int row = m_blk * 2 * BM + rloc;
+            const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+            if (head) {
+                if (lane == 0) {
+                    const long long tw0 = clock64();
+                    for (int f = 0; f < nf; ++f) {
+                        int v;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];"
+                                         : "=r"(v)
+                                         : "l"(ws_flag + fslot + f));
+                        } while (v < 8);
+                    }
+                    (void)tw0;
+                }
+                __syncwarp();
+            }
+#pragma unroll 1
+            for (int c = grp; c < TN / 32; c += NG) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+                ptx::tmem_wait_ld();
+                if (plane) {
+                    const int col0 = n_blk * TN + c * 32;
+                    if (row < m && col0 < n) {
+                        int32_t* dst = ws + (static_cast<int64_t>(-2 - wslot) * m + row) * n + col0;
+                        if (col0 + 32 <= n && (n & 3) == 0) {
+#pragma unroll
+                            for (int v = 0; v < 8; ++v)
+                                reinterpret_cast<int4*>(dst)[v] =
+                                    make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+                        } else {
+#pragma unroll
+                            for (int e = 0; e < 32; ++e)
+                                if (col0 + e < n) dst[e] = static_cast<int32_t>(r[e]);
+                        }
+                    }
+                    continue;
+                }
+                if (tail) {
+                    // slot layout [chunk][v][256 rows][4]: each store instruction of a warp
+                    // writes 512 contiguous bytes
+                    int4* wp = reinterpret_cast<int4*>(ws + static_cast<int64_t>(wslot) * 256 * TN) +
+                               c * 8 * 256 + rloc;
+#pragma unroll
+                    for (int v = 0; v < 8; ++v)
+                        wp[v * 256] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+                    continue;
+                }
+                for (int f = 0; head && f < nf; ++f) {
+                    const int4* wp =
+                        reinterpret_cast<const int4*>(ws + static_cast<int64_t>(fslot + f) * 256 * TN) +
+                        c * 8 * 256 + rloc;
+#pragma unroll
+                    for (int v = 0; v < 8; ++v) {
+                        const int4 pv = __ldcg(wp + v * 256);
+                        r[4 * v] += pv.x, r[4 * v + 1] += pv.y, r[4 * v + 2] += pv.z, r[4 * v + 3] += pv.w;
+                    }
+                }
+                const int col0 = n_blk * TN + c * 32;
+                if constexpr (EPIB > 0) {
+                    if (tma_y) {  // convert, stage the 32 x 32 block, one TMA tensor store
+                        uint8_t* ep = smem + L::epi_off + (ew * 2 + (echunk & 1)) * EPIB;
+                        ++echunk;
+                        if (lane == 0) ptx::bulk_wait_read_allbut1();
+                        __syncwarp();
+                        constexpr int ESZ = static_cast<int>(sizeof(OT));
+                        uint32_t wv[32 * ESZ / 4];
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) {
+                            const double bv =
+                                bias != nullptr ? load_bias(bias, bias_dt, min(col0 + e, n - 1)) : 0.0;
+                            const OT v = convert_out<OUT>(static_cast<int32_t>(r[e]) - corr, s, bv);
+                            if constexpr (ESZ == 4) {
+                                wv[e] = *reinterpret_cast<const uint32_t*>(&v);
+                            } else {
+                                const uint32_t h = *reinterpret_cast<const uint16_t*>(&v);
+                                wv[e >> 1] = (e & 1) ? (wv[e >> 1] | (h << 16)) : h;
+                            }
+                        }
+                        uint4* dst = reinterpret_cast<uint4*>(ep + lane * 32 * ESZ);
+#pragma unroll
+                        for (int v = 0; v < 8 * ESZ / 4; ++v)
+                            dst[v] = make_uint4(wv[4 * v], wv[4 * v + 1], wv[4 * v + 2], wv[4 * v + 3]);
+                        ptx::fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::tma_store_2d(&tmY, ep, col0, m_blk * 2 * BM + rank * BM + ew * 32);
+                            ptx::bulk_commit();
+                        }
+                        continue;
+                    }
+                }
+                if (row < m && col0 < n) {
+                    const int ncols = min(32, n - col0);
+                    store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
+                                         bias_dt, col0, ncols, vec_ok != 0, corr);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+            if (tail) {  // publish the partial: release at gpu scope, one arrival per warp
+                __threadfence();
+                __syncwarp();
+                if (lane == 0) atomicAdd(ws_flag + wslot, 1);
+            }
+            if (dbg && lane == 0 && ew == 0 && grp == 0) {
+                unsigned long long ge1;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge1));
+                atomicAdd(&g_dbg[blockIdx.x % 296][1], ge1 - ge0);
+                atomicAdd(&g_dbg[blockIdx.x % 296][2], 1ull);
+                atomicAdd(&g_dbg2[blockIdx.x % 296][7], ge1 - gstart);  // epilogue done (ns)
+            }
+            ++it;
+        });
+        if (EPIB > 0 && tma_y && lane == 0) ptx::bulk_wait_all();  // staged output stores
+    };
 
     if (warp == 0 && lane == 0) {
         // ---------------- TMA producer (both CTAs) ----------------
@@ -698,144 +846,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             atomicAdd(&g_dbg[blockIdx.x % 296][4], g1 - g0);  // ns of the MMA loop
         }
     } else if (warp >= 4 && warp < 8) {
-        // ---------------- epilogue (both CTAs: own 128 rows) ----------------
-        const int ew = warp - 4;
-        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
-        int it = 0, echunk = 0;
-        if (EPIB > 0 && tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
-        for_each_seg([&](int tile, int, int, int wslot, int fslot, int nf) {
-            const int m_blk = tile % num_m, n_blk = tile / num_m;
-            const int acc = it % NACC;
-            const uint32_t acc_phase = (it / NACC) & 1;
-            const bool tail = SPLITS && wslot >= 0;    // partial sums -> ws[wslot]
-            const bool head = SPLITS && nf > 0;        // add ws[fslot .. fslot + nf)
-            const bool plane = SPLITS && wslot <= -2;  // split-K: raw partial -> plane -2 - wslot
-            ptx::mbar_wait(&tfull[acc], acc_phase);
-            ptx::tc_fence_after();
-            unsigned long long ge0 = 0;
-            if (dbg && lane == 0 && ew == 0) {
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
-                atomicAdd(&g_dbg2[blockIdx.x % 296][6], ge0 - gstart);  // tfull reached (ns)
-            }
-            const int rloc = rank * BM + ew * 32 + lane;  // row within the 256-row tile
-            const int row = m_blk * 2 * BM + rloc;
-            const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-            if (head) {
-                if (lane == 0) {
-                    const long long tw0 = clock64();
-                    for (int f = 0; f < nf; ++f) {
-                        int v;
-                        do {
-                            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];"
-                                         : "=r"(v)
-                                         : "l"(ws_flag + fslot + f));
-                        } while (v < 8);
-                    }
-                    (void)tw0;
-                }
-                __syncwarp();
-            }
-#pragma unroll 1
-            for (int c = 0; c < TN / 32; ++c) {
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
-                ptx::tmem_wait_ld();
-                if (plane) {
-                    const int col0 = n_blk * TN + c * 32;
-                    if (row < m && col0 < n) {
-                        int32_t* dst = ws + (static_cast<int64_t>(-2 - wslot) * m + row) * n + col0;
-                        if (col0 + 32 <= n && (n & 3) == 0) {
-#pragma unroll
-                            for (int v = 0; v < 8; ++v)
-                                reinterpret_cast<int4*>(dst)[v] =
-                                    make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (col0 + e < n) dst[e] = static_cast<int32_t>(r[e]);
-                        }
-                    }
-                    continue;
-                }
-                if (tail) {
-                    // slot layout [chunk][v][256 rows][4]: each store instruction of a warp
-                    // writes 512 contiguous bytes
-                    int4* wp = reinterpret_cast<int4*>(ws + static_cast<int64_t>(wslot) * 256 * TN) +
-                               c * 8 * 256 + rloc;
-#pragma unroll
-                    for (int v = 0; v < 8; ++v)
-                        wp[v * 256] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-                    continue;
-                }
-                for (int f = 0; head && f < nf; ++f) {
-                    const int4* wp =
-                        reinterpret_cast<const int4*>(ws + static_cast<int64_t>(fslot + f) * 256 * TN) +
-                        c * 8 * 256 + rloc;
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) {
-                        const int4 pv = __ldcg(wp + v * 256);
-                        r[4 * v] += pv.x, r[4 * v + 1] += pv.y, r[4 * v + 2] += pv.z, r[4 * v + 3] += pv.w;
-                    }
-                }
-                const int col0 = n_blk * TN + c * 32;
-                if constexpr (EPIB > 0) {
-                    if (tma_y) {  // convert, stage the 32 x 32 block, one TMA tensor store
-                        uint8_t* ep = smem + L::epi_off + (ew * 2 + (echunk & 1)) * EPIB;
-                        ++echunk;
-                        if (lane == 0) ptx::bulk_wait_read_allbut1();
-                        __syncwarp();
-                        constexpr int ESZ = static_cast<int>(sizeof(OT));
-                        uint32_t wv[32 * ESZ / 4];
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) {
-                            const double bv =
-                                bias != nullptr ? load_bias(bias, bias_dt, min(col0 + e, n - 1)) : 0.0;
-                            const OT v = convert_out<OUT>(static_cast<int32_t>(r[e]) - corr, s, bv);
-                            if constexpr (ESZ == 4) {
-                                wv[e] = *reinterpret_cast<const uint32_t*>(&v);
-                            } else {
-                                const uint32_t h = *reinterpret_cast<const uint16_t*>(&v);
-                                wv[e >> 1] = (e & 1) ? (wv[e >> 1] | (h << 16)) : h;
-                            }
-                        }
-                        uint4* dst = reinterpret_cast<uint4*>(ep + lane * 32 * ESZ);
-#pragma unroll
-                        for (int v = 0; v < 8 * ESZ / 4; ++v)
-                            dst[v] = make_uint4(wv[4 * v], wv[4 * v + 1], wv[4 * v + 2], wv[4 * v + 3]);
-                        ptx::fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            ptx::tma_store_2d(&tmY, ep, col0, m_blk * 2 * BM + rank * BM + ew * 32);
-                            ptx::bulk_commit();
-                        }
-                        continue;
-                    }
-                }
-                if (row < m && col0 < n) {
-                    const int ncols = min(32, n - col0);
-                    store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
-                                         bias_dt, col0, ncols, vec_ok != 0, corr);
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
-            if (tail) {  // publish the partial: release at gpu scope, one arrival per warp
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) atomicAdd(ws_flag + wslot, 1);
-            }
-            if (dbg && lane == 0 && ew == 0) {
-                unsigned long long ge1;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge1));
-                atomicAdd(&g_dbg[blockIdx.x % 296][1], ge1 - ge0);
-                atomicAdd(&g_dbg[blockIdx.x % 296][2], 1ull);
-                atomicAdd(&g_dbg2[blockIdx.x % 296][7], ge1 - gstart);  // epilogue done (ns)
-            }
-            ++it;
-        });
-        if (EPIB > 0 && tma_y && lane == 0) ptx::bulk_wait_all();  // staged output stores
+        run_epilogue(warp - 4, 0);
     } else if (L::packed && warp >= 8) {
         // ---------------- int4 -> int8 unpack warps (both CTAs) ----------------
         const int team = (warp - 8) / L::team_warps;
@@ -888,6 +899,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                 }
             }
         });
+        if constexpr (NG > 1) run_epilogue(warp & 3, 1 + (warp - 8) / 4);
+    } else if (!L::packed && NG > 1 && warp >= 8) {
+        run_epilogue(warp & 3, 1 + (warp - 8) / 4);
     }
     ptx::tc_fence_before();
     ptx::cluster_sync();
@@ -1566,7 +1580,7 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
     }
     CUtensorMap ty;
     std::memset(&ty, 0, sizeof(ty));
-    const bool tma_y = epi_block_bytes<OUT>() > 0 && vec && sk < 2;
+    const bool tma_y = epi_block_bytes<OUT>() > 0 && vec && sk < 2 && L::epi_groups == 1;
     if (tma_y) {
         const CUtensorMapDataType dt =
             esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
