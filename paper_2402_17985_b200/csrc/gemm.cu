@@ -594,7 +594,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 8 * NG);
+            ptx::mbar_init(&tempty[a], 8 * (L::packed ? 1 : NG));
         }
         ptx::fence_barrier_init();
     }
@@ -611,11 +611,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     // Lane quarter ew of TMEM; group grp of NG takes chunks grp, grp + NG, ...
     // (with one accumulator, NB = 2, the unpack warps / spare warps join after
     // the main loop so the exposed drain is split NG ways).
+    // Helpers (grp > 0): with packed operands the unpack warps only reach the
+    // epilogue after their whole loop, so they help on the cluster's LAST tile
+    // and never arrive on tempty (nothing reuses the accumulator after it);
+    // spare warps (int8 operands) help on every tile and arrive.
+    constexpr bool HELP_ALL = !L::packed;
     auto run_epilogue = [&](const int ew, const int grp) {
         const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
         int it = 0, echunk = 0;
         if (EPIB > 0 && tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
         for_each_seg([&](int tile, int, int, int wslot, int fslot, int nf) {
+            const bool last = tile + ncl >= num_tiles || (SPLITS && sk != 0);
+            const int ng = (HELP_ALL || last) ? NG : 1;  // groups sharing this tile's chunks
+            if (grp >= ng) {  // a helper skips this tile (keeps the phase count)
+                ++it;
+                return;
+            }
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const int acc = it % NACC;
             const uint32_t acc_phase = (it / NACC) & 1;
@@ -649,7 +660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                 __syncwarp();
             }
 #pragma unroll 1
-            for (int c = grp; c < TN / 32; c += NG) {
+            for (int c = grp; c < TN / 32; c += ng) {
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
                 ptx::tmem_wait_ld();
@@ -732,7 +743,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
+            if (lane == 0 && (HELP_ALL || grp == 0))
+                ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
             if (tail) {  // publish the partial: release at gpu scope, one arrival per warp
                 __threadfence();
                 __syncwarp();

@@ -86,3 +86,17 @@ def test_sweep_8192_int8(port, fq, m):
     y16 = layer.forward(xt, out_dtype=torch.float16).cpu().numpy()
     rows = np.sort(np.random.default_rng(m).choice(m, min(m, 6), replace=False))
     check_rows(port, L, x, acc, y16, rows)
+
+
+def test_llama13b_up_full_batch_int4(port, fq):
+    """configs[3] at M = 2048 on one GPU: 216 tiles of 256 x 512 on 74 CTA pairs
+    (several tiles per pair with the single-accumulator epilogue and int4 unpack)."""
+    import torch
+
+    k, n, m = 5120, 13824, 2048
+    L, cfg, x, xt, a_fmt, b_fmt = layer_case(port, fq, k, n, m, 4, index=13)
+    layer = fq.Layer(cfg, a_format=a_fmt, b_format=b_fmt)
+    acc = layer.forward(xt, out_dtype=torch.int32).cpu().numpy()
+    y16 = layer.forward(xt, out_dtype=torch.float16).cpu().numpy()
+    rows = np.sort(np.random.default_rng(5).choice(m, 8, replace=False))
+    check_rows(port, L, x, acc, y16, rows)
