@@ -467,7 +467,7 @@ struct PairLayout {
     static constexpr int raw_stage = a_raw + b_raw;
     static constexpr int direct_bytes = (APK ? 0 : a_raw) + (BPK ? 0 : b_raw);
     static constexpr int packed_bytes = (APK ? a_raw : 0) + (BPK ? b_raw : 0);
-    static constexpr int USTAGES = packed ? (NB == 1 ? 4 : 2) : 0;
+    static constexpr int USTAGES = packed ? (NB == 1 ? 4 : 3) : 0;
     static constexpr int a_unp = APK ? BM * BK : 0;
     static constexpr int b_unp = BPK ? NB * (BN / 2) * BK : 0;
     static constexpr int unp_stage = a_unp + b_unp;
@@ -1684,7 +1684,7 @@ constexpr int fit_stages(int maxst) {
 
 template <int AF, int BF, int NB, int OUT>
 void launch_pair_fit(const GemmArgs& g, cudaStream_t s) {
-    constexpr int ST = fit_stages<AF != F8, BF != F8, NB, epi_block_bytes<OUT>()>(NB == 1 ? 6 : 4);
+    constexpr int ST = fit_stages<AF != F8, BF != F8, NB, epi_block_bytes<OUT>()>(6);
     static_assert(ST >= 2, "pipeline depth");
     launch_pair<ST, OUT, AF, BF, NB>(g, s);
 }
