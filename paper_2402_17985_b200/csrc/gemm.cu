@@ -193,9 +193,9 @@ __device__ __forceinline__ void store_row_chunk(void* y, int64_t base, uint32_t 
             }
             uint4* p = reinterpret_cast<uint4*>(static_cast<uint16_t*>(y) + base);
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                p[q] = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
-                                  packed[4 * q + 3]);
+            for (int q = 0; q < 4; ++q)  // streaming stores: the output is not re-read here
+                __stcs(p + q, make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
+                                         packed[4 * q + 3]));
             return;
         }
     }
@@ -662,8 +662,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
 #pragma unroll 1
             for (int c = grp; c < TN / 32; c += ng) {
                 uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
-                ptx::tmem_wait_ld();
+                if (!(dbg & 8)) {
+                    ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+                    ptx::tmem_wait_ld();
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) r[e] = static_cast<uint32_t>(c + e);
+                }
                 if (plane) {
                     const int col0 = n_blk * TN + c * 32;
                     if (row < m && col0 < n) {
@@ -735,7 +740,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                         continue;
                     }
                 }
-                if (row < m && col0 < n) {
+                if (row < m && col0 < n && !(dbg & 4)) {
                     const int ncols = min(32, n - col0);
                     store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
                                          bias_dt, col0, ncols, vec_ok != 0, corr);
