@@ -217,7 +217,21 @@ struct K16Params {
     int dbg;
 };
 
-__device__ unsigned long long g_k1dbg[16];  // FQG_K1_DEBUG: summed phase end times (cycles)
+__device__ unsigned long long g_k1dbg[16];
+
+// Extension pieces 1 .. last of one element into d[0 .. last): full pieces
+// (value fv) for p < ce, the remainder qe at p == ce (flatten.cpp:71-72);
+// word stores for the aligned middle of the full-piece run.
+__device__ __forceinline__ void fill_pieces(int8_t* d, int last, int ce, int fv, int qe) {
+    const int nfull = min(ce - 1, last);
+    const uint32_t word = (static_cast<uint32_t>(fv) & 0xFFu) * 0x01010101u;
+    int p = 0;
+    for (; p < nfull && (reinterpret_cast<uintptr_t>(d + p) & 3u) != 0u; ++p)
+        d[p] = static_cast<int8_t>(fv);
+    for (; p + 4 <= nfull; p += 4) *reinterpret_cast<uint32_t*>(d + p) = word;
+    for (; p < nfull; ++p) d[p] = static_cast<int8_t>(fv);
+    if (ce <= last) d[ce - 1] = static_cast<int8_t>(qe);
+}  // FQG_K1_DEBUG: summed phase end times (cycles)
 
 template <int TW>
 __device__ __forceinline__ void team_sync(int team) {
@@ -304,9 +318,14 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
     mark(0);
 
     unsigned long long sat = 0;
+    // Row sum of the final operand, kept incrementally (tier-1 words, tier-2
+    // corrections and extension pieces, plan_w copies) instead of a re-read pass.
+    const bool want_rs = p.rowsum != nullptr;
+    int rs_run = 0;
     // Row start: the team's previous bulk store has read fl / pk; zero the
     // plan_x extension slots [K, C1); fetch the hot channels' x values.
     auto row_begin = [&](int row) {
+        rs_run = 0;
         if (tt == 0) ptx::bulk_wait_read_all();
         team_sync<TW>(team);
         const int z0 = (k + 15) & ~15;
@@ -335,9 +354,13 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
                 bq[2 * e] = __float_as_uint(__fmaf_rn(f.x, cc[2 * e], kMagic));
                 bq[2 * e + 1] = __float_as_uint(__fmaf_rn(f.y, cc[2 * e + 1], kMagic));
             }
-            *reinterpret_cast<uint2*>(fl + 8 * g) =
-                make_uint2(pack_lowbytes(bq[0], bq[1], bq[2], bq[3]),
-                           pack_lowbytes(bq[4], bq[5], bq[6], bq[7]));
+            const uint32_t wlo = pack_lowbytes(bq[0], bq[1], bq[2], bq[3]);
+            const uint32_t whi = pack_lowbytes(bq[4], bq[5], bq[6], bq[7]);
+            *reinterpret_cast<uint2*>(fl + 8 * g) = make_uint2(wlo, whi);
+            if (want_rs) {
+                rs_run = __dp4a(static_cast<int>(wlo), 0x01010101, rs_run);
+                rs_run = __dp4a(static_cast<int>(whi), 0x01010101, rs_run);
+            }
             if (const uint32_t hg = static_cast<uint32_t>(shotg[g]); (hg & 0xFFu) != 0u) {
                 uint32_t hm = hg & 0xFFu;  // hot channels of the group: keep their x for tier 2
                 int hi = static_cast<int>(hg >> 8);
@@ -390,10 +413,12 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
                 int ce, qe, fv;
                 const int cap_e = __ldg(p.cap + j);
                 exact(j, xb, cap_e, __ldg(p.rs32 + j), ce, qe, fv);
-                fl[j] = static_cast<int8_t>(ce >= 1 ? fv : qe);
+                const int v0 = ce >= 1 ? fv : qe;
+                if (want_rs) rs_run += v0 - fl[j];
+                fl[j] = static_cast<int8_t>(v0);
                 const int last = ce >= 1 ? min(ce, cap_e - 1) : 0;
-                int8_t* ext = fl + k + __ldg(p.off + j) - 1;
-                for (int q = 1; q <= last; ++q) ext[q] = static_cast<int8_t>(q < ce ? fv : qe);
+                fill_pieces(fl + k + __ldg(p.off + j), last, ce, fv, qe);
+                if (want_rs && ce >= 1) rs_run += min(ce - 1, last) * fv + (ce <= last ? qe : 0);
             }
         }
         const int nitems = p.nhot + (overflow ? 0 : nq);
@@ -413,32 +438,17 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
             }
             int ce, qe, fv;
             exact(j, xb, cap_e, rs32_j, ce, qe, fv);
-            fl[j] = static_cast<int8_t>(ce >= 1 ? fv : qe);  // slot j = piece 0
+            const int v0 = ce >= 1 ? fv : qe;
+            if (want_rs) rs_run += v0 - fl[j];  // tier 1 left its (replaced) byte in slot j
+            fl[j] = static_cast<int8_t>(v0);  // slot j = piece 0
             if (ce >= 1) {  // pieces 1 .. E -> the (zeroed) extension slots
                 const int last = min(ce, cap_e - 1);
-                const int ext0 = k + off_j - 1;
-                int slot = kRunCap;
-                if (last > kInline) slot = atomicAdd(&nrun, 1);
-                if (slot < kRunCap)
-                    runs[slot] = make_uint4(static_cast<uint32_t>(ext0), static_cast<uint32_t>(last),
-                                            static_cast<uint32_t>(ce),
-                                            (static_cast<uint32_t>(fv) & 0xFFu) |
-                                                ((static_cast<uint32_t>(qe) & 0xFFu) << 8));
-                else
-                    for (int q = 1; q <= last; ++q) fl[ext0 + q] = static_cast<int8_t>(q < ce ? fv : qe);
+                fill_pieces(fl + k + off_j, last, ce, fv, qe);
+                if (want_rs) rs_run += min(ce - 1, last) * fv + (ce <= last ? qe : 0);
             }
         }
         team_sync<TW>(team);
         mark(2);
-        const int nr = min(nrun, kRunCap);
-        for (int ri = 0; ri < nr; ++ri) {  // long runs: the team over one run's bytes
-            const uint4 rr = runs[ri];
-            const int8_t v_full = static_cast<int8_t>(rr.w & 0xFFu);
-            const int8_t v_rem = static_cast<int8_t>((rr.w >> 8) & 0xFFu);
-            for (int q = 1 + tt; q <= static_cast<int>(rr.y); q += TW)
-                fl[rr.x + q] = q < static_cast<int>(rr.z) ? v_full : v_rem;
-        }
-        team_sync<TW>(team);
         if (tt == 0) qlen = 0, nrun = 0;
         mark(3);
         // plan_w copies [C1, K'): byte gathers from the flattened row
@@ -447,33 +457,26 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
             const int4 sv = swsrc[u];
             const uint32_t b0 = static_cast<uint8_t>(fl[sv.x]), b1 = static_cast<uint8_t>(fl[sv.y]);
             const uint32_t b2 = static_cast<uint8_t>(fl[sv.z]), b3 = static_cast<uint8_t>(fl[sv.w]);
-            *reinterpret_cast<uint32_t*>(fl + c1 + 4 * u) =
+            const uint32_t wv =
                 __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+            *reinterpret_cast<uint32_t*>(fl + c1 + 4 * u) = wv;
+            if (want_rs) rs_run = __dp4a(static_cast<int>(wv), 0x01010101, rs_run);
         }
-        if (PACK4 || p.rowsum != nullptr) {
+        if constexpr (PACK4) {  // byte i = q[i] & 15 | q[16 + i] << 4
             team_sync<TW>(team);
-            int rsum = 0;
             for (int u = tt; u < (kp >> 5); u += TW) {
                 const uint4 lo = *reinterpret_cast<const uint4*>(fl + 32 * u);
                 const uint4 hi = *reinterpret_cast<const uint4*>(fl + 32 * u + 16);
-                rsum = __dp4a(static_cast<int>(lo.x), 0x01010101, rsum);
-                rsum = __dp4a(static_cast<int>(lo.y), 0x01010101, rsum);
-                rsum = __dp4a(static_cast<int>(lo.z), 0x01010101, rsum);
-                rsum = __dp4a(static_cast<int>(lo.w), 0x01010101, rsum);
-                rsum = __dp4a(static_cast<int>(hi.x), 0x01010101, rsum);
-                rsum = __dp4a(static_cast<int>(hi.y), 0x01010101, rsum);
-                rsum = __dp4a(static_cast<int>(hi.z), 0x01010101, rsum);
-                rsum = __dp4a(static_cast<int>(hi.w), 0x01010101, rsum);
-                if constexpr (PACK4)  // byte i = q[i] & 15 | q[16 + i] << 4
-                    *reinterpret_cast<uint4*>(pk + 16 * u) =
-                        make_uint4(pack_i4_word(lo.x, hi.x), pack_i4_word(lo.y, hi.y),
-                                   pack_i4_word(lo.z, hi.z), pack_i4_word(lo.w, hi.w));
+                *reinterpret_cast<uint4*>(pk + 16 * u) =
+                    make_uint4(pack_i4_word(lo.x, hi.x), pack_i4_word(lo.y, hi.y),
+                               pack_i4_word(lo.z, hi.z), pack_i4_word(lo.w, hi.w));
             }
-            if (p.rowsum != nullptr) {
+        }
+        if (want_rs) {
+            int rsum = rs_run;
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-                if (lane == 0) atomicAdd(&rsum_t, rsum);
-            }
+            for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
+            if (lane == 0) atomicAdd(&rsum_t, rsum);
         }
         ptx::fence_proxy_async_smem();
         team_sync<TW>(team);
