@@ -606,7 +606,7 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
             unsigned long long h[16];
             FQG_CUDA(cudaDeviceSynchronize());
             FQG_CUDA(cudaMemcpyFromSymbol(h, g_k1dbg, sizeof(h)));
-            const double nt = static_cast<double>(grid) * (kWarps * 32 / 32);
+            const double nt = static_cast<double>(grid) * (kWarps * 32 / TW);  // team leaders
             std::fprintf(stderr,
                          "[fqg k1] avg cycles since start per team: staged %.0f, row_begin done "
                          "%.0f, tier1 done %.0f, tier2 done %.0f, runs done %.0f, copies done %.0f, "
