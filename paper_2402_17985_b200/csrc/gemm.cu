@@ -482,8 +482,10 @@ struct PairLayout {
     // epilogue warp groups (4 warps each): NB = 2 drains its single accumulator
     // after the main loop with the unpack warps (or 4 spare warps) joining in
     // (4-byte outputs keep one group and the staged TMA-store epilogue instead)
-    static constexpr int epi_groups = (NB == 2 && EPIB != 32 * 32 * 4) ? (packed ? 3 : 2) : 1;
-    static constexpr int threads = 256 + 32 * (packed ? unpack_warps : (epi_groups - 1) * 4);
+    static constexpr int epi_groups = (NB == 2 && EPIB != 32 * 32 * 4) ? (packed ? 3 : 4) : 1;
+    // spare warps (after the unpack warps, if any) that only run epilogue groups
+    static constexpr int spare_warps = (epi_groups - 1) * 4 - (packed && epi_groups > 1 ? unpack_warps : 0);
+    static constexpr int threads = 256 + 32 * (unpack_warps + spare_warps);
     static constexpr int tmem_cols = NB == 1 ? 2 * BN : NB * BN;
     // Arrivals freeing a raw stage in each CTA: the leader's multicast MMA
     // commit when an operand is read straight from the raw stage, plus one per
@@ -624,6 +626,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             const bool last = tile + ncl >= num_tiles || (SPLITS && sk != 0);
             const int ng = (HELP_ALL || last) ? NG : 1;  // groups sharing this tile's chunks
             if (grp >= ng) {  // a helper skips this tile (keeps the phase count)
+                // Spare warps are idle, so they must observe every tfull phase in
+                // order (a parity wait two phases ahead would alias); the unpack
+                // warps only get here after all earlier phases completed.
+                if (warp >= 8 + L::unpack_warps) ptx::mbar_wait(&tfull[it % NACC], (it / NACC) & 1);
                 ++it;
                 return;
             }
@@ -864,7 +870,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
         }
     } else if (warp >= 4 && warp < 8) {
         run_epilogue(warp - 4, 0);
-    } else if (L::packed && warp >= 8) {
+    } else if (L::packed && warp >= 8 && warp < 8 + L::unpack_warps) {
         // ---------------- int4 -> int8 unpack warps (both CTAs) ----------------
         const int team = (warp - 8) / L::team_warps;
         const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
@@ -917,7 +923,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             }
         });
         if constexpr (NG > 1) run_epilogue(warp & 3, 1 + (warp - 8) / 4);
-    } else if (!L::packed && NG > 1 && warp >= 8) {
+    } else if (NG > 1 && warp >= 8) {  // spare warps: epilogue groups only
         run_epilogue(warp & 3, 1 + (warp - 8) / 4);
     }
     ptx::tc_fence_before();
