@@ -245,6 +245,7 @@ template <bool F16, bool PACK4, int TW>
 __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_constant__ K16Params p) {
     constexpr int TEAMS = kWarps * 32 / TW;
     const long long t_start = clock64();
+    ptx::griddep_launch_dependents();  // K4 may start its prologue (it waits for our stores)
     auto mark = [&](int slot) {
         if (p.dbg && (threadIdx.x % TW) == 0) atomicAdd(&g_k1dbg[slot], clock64() - t_start);
     };

@@ -608,6 +608,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_holder;
+    // Launched as a programmatic dependent of K1: everything above overlapped
+    // K1's tail; A, the row sums and y are touched only after this.
+    ptx::griddep_wait();
 
     // ---------------- epilogue (both CTAs: own 128 rows) ----------------
     // Lane quarter ew of TMEM; group grp of NG takes chunks grp, grp + NG, ...
@@ -1618,10 +1621,25 @@ void launch_pair(const GemmArgs& g, cudaStream_t stream) {
         if (r != CUDA_SUCCESS)
             throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed (" + std::to_string(r) + ")");
     }
-    kern<<<2 * nclusters, L::threads, L::total, stream>>>(
-        ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb, g.scale, g.bias,
-        g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk, ws, ws_flag, ty, tma_y ? 1 : 0);
-    cudaError_t le = cudaGetLastError();
+    static const bool pdl = [] {
+        const char* e = std::getenv("FQG_PDL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * nclusters);
+    cfg.blockDim = dim3(L::threads);
+    cfg.dynamicSmemBytes = L::total;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaError_t le = cudaLaunchKernelEx(
+        &cfg, kern, ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb,
+        g.scale, g.bias, g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk, ws, ws_flag, ty,
+        tma_y ? 1 : 0);
+    if (le == cudaSuccess) le = cudaGetLastError();
     if (le == cudaSuccess && sk >= 2) {
         const int64_t total = g.m * g.n;
         const int rgrid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * num_sms(dev)));
