@@ -258,3 +258,41 @@ def test_gemm_stream_k_shapes(fq, m, n, kp):
                                y.data_ptr(), _lib.I32, n, None, None, _lib.NONE,
                                torch.cuda.current_stream().cuda_stream))
     assert np.array_equal(y.cpu().numpy().astype(np.int64), ref)
+
+
+def _rn_bf16(v):
+    """Round-to-nearest-even of float64 values to bfloat16 (normal range), as float64."""
+    mant, ex = np.frexp(v)
+    return np.ldexp(np.round(mant * 256.0), ex - 8)
+
+
+@pytest.mark.parametrize("sx,sw", [(2.0 ** -10, 1.0), (2.0 ** -14, 0.5), (3.7e-5, 0.0123),
+                                   (1.0 / 3.0, 0.9), (2.0 ** -30, 1.0)])
+@pytest.mark.parametrize("out", ["f16", "bf16"])
+def test_half_outputs_are_rn16_of_reference(fq, sx, sw, out):
+    """2-byte outputs equal RN16(double(acc) * (s_x * s_w)) exactly (quantize.cpp:193-196
+    rounded once). The epilogue's certified fp32 fast path must defer every element
+    near a rounding midpoint: power-of-two scales make ~half of them exact ties;
+    2^-30 puts outputs in the fp16 subnormal range; 0.3 straddles the fp16 maximum."""
+    import torch
+
+    from paper_2402_17985_b200 import _lib
+
+    m, n, kp = 512, 1024, 1536
+    g = torch.Generator().manual_seed(int(sx * 1e6) + n)
+    a = torch.randint(-127, 128, (m, kp), dtype=torch.int8, generator=g)
+    b = torch.randint(-127, 128, (n, kp), dtype=torch.int8, generator=g)
+    acc = a.numpy().astype(np.int64) @ b.numpy().astype(np.int64).T
+    v = acc.astype(np.float64) * (sx * sw)
+    scale = torch.tensor([sx, sw], dtype=torch.float64, device="cuda")
+    tdt = torch.float16 if out == "f16" else torch.bfloat16
+    y = torch.empty((m, n), dtype=tdt, device="cuda")
+    fq.check(fq.lib().fqg_gemm(a.cuda().data_ptr(), _lib.I8, kp, b.cuda().data_ptr(), _lib.I8, kp,
+                               m, n, kp, y.data_ptr(), _lib.F16 if out == "f16" else _lib.BF16, n,
+                               scale.data_ptr(), None, _lib.NONE,
+                               torch.cuda.current_stream().cuda_stream))
+    got = y.double().cpu().numpy()
+    want = v.astype(np.float16).astype(np.float64) if out == "f16" else _rn_bf16(v)
+    bad = np.argwhere(got != want)
+    assert bad.size == 0, f"{len(bad)} mismatches, e.g. acc {acc[tuple(bad[0])]}: " \
+                          f"{got[tuple(bad[0])]} vs {want[tuple(bad[0])]}"
