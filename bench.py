@@ -366,7 +366,8 @@ def main():
                 "tokens_per_s": m / t_e2e,
                 "h2d_bytes_per_step": m * k * 8, "d2h_bytes_per_step": m * (b1 - b0) * 8 + 8,
                 "api": "fqg_layer_run_host (drop-in fq::run_layer, f64 host buffers, pinned)"},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches_per_step * args.steps,  # the headline (one-graph) loop;
+        # the per-kernel loop launches the same number again
         "launch": "one CUDA graph per step (K1, then K4 as a programmatic dependent launch); "
                   "K1 and K4 also timed apart from their own graphs for the rooflines",
         "clocks": clk.summary(),
