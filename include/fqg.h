@@ -155,6 +155,16 @@ int fqg_gemm(const void* a_dev, int a_fmt, int64_t lda, const void* b_dev, int b
              int64_t m, int64_t n, int64_t kp, void* y_dev, int y_dtype, int64_t ldy,
              const double* scale_dev, const void* bias_dev, int bias_dtype, void* stream);
 
+/* The launch fqg_gemm (and a layer's GEMM) makes for a shape, on the current
+ * device; host-only query for tests and tooling. kernel 1: 1-CTA 128 x tile_n
+ * tiles; kernel 2: CTA pair (cta_group::2) 256 x tile_n tiles; splits >= 2:
+ * split-K into INT32 planes plus a reduce/epilogue kernel; ctas: grid size. */
+typedef struct fqg_gemm_plan_info {
+    int kernel, tile_m, tile_n, splits, ctas;
+} fqg_gemm_plan_info;
+int fqg_gemm_plan(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int y_dtype,
+                  fqg_gemm_plan_info* out);
+
 /* Host-side plan arithmetic (pure integer/FP64 work, no device):
  * fq::build_flatten_plan (flatten.cpp:17-45). e/off: [k]. */
 int fqg_build_flatten_plan(const double* maxes, int64_t k, double t, int64_t block, int64_t* e,

@@ -142,6 +142,7 @@ class Port:
                                                 C.POINTER(Port._L)]
         L.fqo_layer_free.argtypes = [C.POINTER(Port._L)]
         L.fqo_run_layer.argtypes = [C.POINTER(Port._L), _f64p, I64, _f64p, C.POINTER(I64), P, P]
+        L.fqo_quantize_acts.argtypes = [C.POINTER(Port._L), _f64p, I64, P, C.POINTER(I64)]
 
     # -- flatten.cpp -----------------------------------------------------
     def split(self, a: float, t: float) -> tuple[int, float]:
@@ -253,6 +254,27 @@ class Port:
         return Port._L(layer.bits, layer.k, layer.n, _ptr(s), layer.t_x, layer.t_w, _ptr(ex),
                        _ptr(ew), layer.c1, layer.kp, layer.block, _ptr(wq), layer.s_w,
                        layer.act_scale)
+
+    def quantize_acts(self, layer: Layer, x):
+        """The activation half of run_layer (pipeline.cpp:164-167): (qx int32 [M,K'], sat)."""
+        x = np.ascontiguousarray(x, np.float64)
+        if x.shape[1] != layer.k:
+            raise InvalidArgument("run_layer: input channel count does not match recipe")
+        keep: list = []
+        L = self._as_struct(layer, keep)
+        qx = np.zeros((x.shape[0], layer.kp), np.int32)
+        sat = I64()
+        _check(self.lib.fqo_quantize_acts(C.byref(L), x, x.shape[0], _ptr(qx), C.byref(sat)),
+               "quantize_acts")
+        return qx, sat.value
+
+    @staticmethod
+    def exact_acc(qx, wq):
+        """int_matmul_raw (quantize.cpp:166-188) for full-size checks: an f64 BLAS
+        product of the integer operands. Exact, in any summation order, because
+        every partial sum is an integer below 2^53 (|acc| <= K' * 127^2)."""
+        assert qx.shape[1] * 127 * 127 < 2 ** 53
+        return (qx.astype(np.float64) @ wq.astype(np.float64)).astype(np.int64)
 
     def run_layer(self, layer: Layer, x, debug: bool = False):
         """Returns (y f64 [M,N], saturation) or, with debug, (y, sat, qx int32, acc int64)."""

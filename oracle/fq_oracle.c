@@ -441,9 +441,11 @@ fail:
 }
 
 /* pipeline.cpp:159-169 */
-int fqo_run_layer(const fqo_layer* l, const double* x, int64_t m, double* y, int64_t* sat,
-                  int32_t* qx_out, int64_t* acc_out) {
-    const int64_t k = l->k, c1 = l->c1, kp = l->kp, n = l->n;
+/* The activation half of run_layer (pipeline.cpp:164-167): divide_columns ->
+ * flatten_tensor (saturating) -> repeat_columns -> quantize_per_tensor with the
+ * static act_scale. qx: M*K' int32. */
+int fqo_quantize_acts(const fqo_layer* l, const double* x, int64_t m, int32_t* qx, int64_t* sat) {
+    const int64_t k = l->k, c1 = l->c1, kp = l->kp;
     int rc;
     double* divided = malloc(sizeof(double) * (size_t)(m * k));
     fqo_divide_columns(x, m, k, l->s, divided);
@@ -454,9 +456,18 @@ int fqo_run_layer(const fqo_layer* l, const double* x, int64_t m, double* y, int
     double* rep = malloc(sizeof(double) * (size_t)(m * kp));
     fqo_repeat_columns(flat, m, c1, l->e_w, l->block, rep);
     free(flat);
-    int32_t* qx = qx_out ? qx_out : malloc(sizeof(int32_t) * (size_t)(m * kp));
     rc = rc ? rc : fqo_quantize_per_tensor(rep, m * kp, l->bits, l->act_scale, qx, NULL);
     free(rep);
+    if (sat) *sat = s;
+    return rc;
+}
+
+int fqo_run_layer(const fqo_layer* l, const double* x, int64_t m, double* y, int64_t* sat,
+                  int32_t* qx_out, int64_t* acc_out) {
+    const int64_t kp = l->kp, n = l->n;
+    int32_t* qx = qx_out ? qx_out : malloc(sizeof(int32_t) * (size_t)(m * kp));
+    int64_t s = 0;
+    int rc = fqo_quantize_acts(l, x, m, qx, &s);
     int64_t* acc = acc_out ? acc_out : malloc(sizeof(int64_t) * (size_t)(m * n));
     rc = rc ? rc : fqo_int_matmul_raw(qx, m, kp, l->bits, l->wq, n, l->bits, acc);
     if (!rc) fqo_int_matmul_dequant(acc, m * n, l->act_scale, l->s_w, y);

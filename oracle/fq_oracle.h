@@ -87,6 +87,9 @@ int fqo_quantize_layer_pinned(const double* w, int64_t k, int64_t n, const doubl
                               double beta, int64_t block, int smooth, int clip, fqo_layer* out);
 void fqo_layer_free(fqo_layer* l);
 
+/* pipeline.cpp:164-167, the activation half of run_layer: qx M*K' int32 */
+int fqo_quantize_acts(const fqo_layer* l, const double* x, int64_t m, int32_t* qx, int64_t* sat);
+
 /* pipeline.cpp:159-169 (qx/acc optional debug outputs: M*K' int32, M*N int64) */
 int fqo_run_layer(const fqo_layer* l, const double* x, int64_t m, double* y, int64_t* sat,
                   int32_t* qx_out, int64_t* acc_out);

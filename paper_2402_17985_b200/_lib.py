@@ -93,6 +93,10 @@ class SynthOpts(C.Structure):
     ]
 
 
+class GemmPlan(C.Structure):
+    _fields_ = [("kernel", INT), ("tile_m", INT), ("tile_n", INT), ("splits", INT), ("ctas", INT)]
+
+
 # Every symbol include/fqg.h declares, with its ctypes signature.
 SIGNATURES = {
     "fqg_last_error": (C.c_char_p, []),
@@ -108,6 +112,7 @@ SIGNATURES = {
     "fqg_layer_quantize_acts_ex": (INT, [P, P, INT, I64, P, P, P, P]),
     "fqg_layer_gemm_ex": (INT, [P, P, P, I64, P, INT, I64, P, INT, P]),
     "fqg_gemm": (INT, [P, INT, I64, P, INT, I64, I64, I64, I64, P, INT, I64, P, P, INT, P]),
+    "fqg_gemm_plan": (INT, [I64, I64, I64, INT, INT, INT, C.POINTER(GemmPlan)]),
     "fqg_build_flatten_plan": (INT, [P, I64, F64_, I64, P, P, C.POINTER(I64), C.POINTER(I64)]),
     "fqg_split_against_threshold": (None, [F64_, F64_, C.POINTER(I64), C.POINTER(F64_)]),
     "fqg_recipe_plan": (INT, [P, I64, I64, P, INT, F64_, F64_, I64, INT, INT, P,

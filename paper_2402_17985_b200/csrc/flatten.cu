@@ -216,6 +216,7 @@ __global__ void __launch_bounds__(256, 4)
     // clear of a rounding half-integer (tools/verify_fp32_split.c, tier 1).
     const float ras32 = static_cast<float>(sc.ras);
     const float qlo = sc.q32 * (1.0f - 4e-7f);
+    const int qmaxi = static_cast<int>(sc.qmax);
     unsigned long long sat = 0;
     for (int j0 = threadIdx.x * 8; j0 < k; j0 += blockDim.x * 8) {
         const int nj = min(8, k - j0);
@@ -237,7 +238,9 @@ __global__ void __launch_bounds__(256, 4)
                 const float dd = fabsf(__fsub_rn(__fsub_rn(tz, qf), 0.5f));  // |frac - 1/2|
                 const float lim = __fsub_rn(0.5f, __fadd_rn(__fmul_rn(z, 4e-7f), 1e-6f));
                 const bool ok = z < qlo && dd < lim;
-                const int qi = static_cast<int>(qf);
+                // clamp (quantize.cpp:44-45): act_scale and T_x are independent recipe
+                // fields, so z may exceed qmax when act_scale * qmax < T_x
+                const int qi = min(static_cast<int>(qf), qmaxi);
                 const uint32_t byte =
                     ok ? static_cast<uint32_t>((xf[e] < 0.0f ? -qi : qi) & 0xFF) : 0u;
                 if (e < 4)

@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -41,6 +42,19 @@ inline int dtype_size(int dt) {
 }
 
 int num_sms(int device);
+
+// The dynamic shared-memory limit is a per-device function attribute: set it
+// once per (kernel, device), not once per process.
+template <auto Kern>
+void ensure_smem_attr(int bytes) {
+    static std::atomic<uint64_t> done{0};
+    int dev = 0;
+    FQG_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return;
+    FQG_CUDA(cudaFuncSetAttribute(Kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done.fetch_or(bit, std::memory_order_acq_rel);
+}
 
 extern thread_local std::string g_last_error;
 
@@ -84,8 +98,18 @@ struct GemmArgs {
     int bias_dtype;
     int variant = 0;      // 0 auto, 1 single-CTA kernel, 2 CTA-pair kernel
     const int32_t* rowsum = nullptr;  // [M] sum of each A row (FQG_I4_BIASED weights)
+    int qmax_a = 0, qmax_b = 0;       // operand value bounds (0: from the format)
 };
 void gemm_i8(const GemmArgs& g, cudaStream_t stream);
+
+// The launch gemm_i8 makes for a shape (fqg_gemm_plan exposes it).
+struct GemmPlan {
+    int kernel = 0;           // 1: 1-CTA 128 x tile_n tiles; 2: CTA pair 256 x tile_n
+    int tile_m = 0, tile_n = 0;
+    int splits = 0;           // >= 2: split-K planes + k_splitk_reduce
+    int ctas = 0;             // grid size
+};
+GemmPlan plan_gemm(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int variant, int sms);
 
 // TMA descriptor construction through the driver entry point (no -lcuda).
 void make_tmap_2d_u8(CUtensorMap* map, const void* base, uint64_t inner_bytes, uint64_t rows,

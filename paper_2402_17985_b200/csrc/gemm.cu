@@ -1,1946 +1,30 @@
-// gemm.cu — K4: the flattened low-bit GEMM on 5th-gen tensor cores.
-//
-//   Y[M,N] = epi( sum_k A[M,k] * B[N,k] ),  A,B int8 K-major, INT32 accumulate
-//
-// replaces fq::int_matmul_raw + fq::int_matmul (quantize.cpp:166-198). The
-// accumulators are exact int32 (|acc| <= K' * qmax^2 < 2^31 for K' <= 133144,
-// checked by the host), so the result is bit-identical to the reference's
-// int64 sums; the epilogue then forms y = double(acc) * (s_x * s_w) exactly as
-// quantize.cpp:193-196 does and rounds once to the output type.
-//
-// Structure (one CTA per SM, persistent over output tiles, 256 threads):
-//   warp 0 lane 0 : TMA producer — A tile 128x128B and B tile BNx128B per stage,
-//                   128-byte swizzle, OOB rows/cols zero-filled by the TMA unit
-//   warp 1        : TMEM allocator (2*BN columns: double-buffered accumulator);
-//                   lane 0 issues tcgen05.mma.cta_group::1.kind::i8 128xBNx32
-//   warps 4..7    : epilogue — tcgen05.ld 32x32b, dequant + bias, convert, store
-// Pipelines: smem ring full/empty mbarriers (TMA <-> MMA, tcgen05.commit frees a
-// slot), TMEM full/empty mbarriers (MMA <-> epilogue), so the epilogue of tile
-// i overlaps the main loop of tile i+1.
-#include <cuda_bf16.h>
-#include <cuda_fp16.h>
-#include <cudaTypedefs.h>
-
-#include <algorithm>
-#include <type_traits>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <mutex>
-
-#include "fqg_internal.h"
-#include "ptx.cuh"
+// gemm.cu — K4 host side: the launch plan (tile shape, split-K) and the
+// dispatch to the per-format kernel translation units (gemm_pair_*.cu,
+// gemm_one_*.cu; the kernels themselves are in gemm_kernels.cuh).
+#include "gemm_kernels.cuh"
 
 namespace fqg {
+void gemm_pair_F8_F8(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
+void gemm_pair_F8_FS4(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
+void gemm_pair_F8_FU4(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
+void gemm_pair_FS4_F8(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
+void gemm_pair_FS4_FS4(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
+void gemm_pair_FS4_FU4(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
+void gemm_one_F8(const GemmArgs& g, int bn, cudaStream_t s);
+void gemm_one_FS4(const GemmArgs& g, int bn, cudaStream_t s);
+
 namespace {
-
-constexpr int BM = 128;       // UMMA M (cta_group::1)
-// Operand formats inside the kernels: int8 bytes, signed packed int4 (FQG_I4),
-// or biased packed int4 (stored nibble = q + 8, the layer's weight format: it
-// unpacks with one AND per 4 values and is fed to the MMA as UNSIGNED int8;
-// the epilogue subtracts 8 * rowsum(A) per output row, exact in int32).
-constexpr int F8 = 0, FS4 = 1, FU4 = 2;
-constexpr int BK = 128;       // K bytes per stage = one 128B swizzle row
-constexpr int UK = 32;        // K per tcgen05.mma kind::i8
-
-// Shared-memory plan. The "raw" ring is what the TMA writes: int8 operands in
-// the 128B-swizzled UMMA layout, packed int4 operands as plain 64-byte rows.
-// With a packed operand, unpack warps expand it into the "unpacked" ring
-// (int8, 128B-swizzled) before the MMA reads it.
-template <int BN, int STAGES, bool APK, bool BPK>
-struct Layout {
-    static constexpr bool packed = APK || BPK;
-    static constexpr int a_raw = APK ? BM * BK / 2 : BM * BK;
-    static constexpr int b_raw = BPK ? BN * BK / 2 : BN * BK;
-    static constexpr int raw_stage = a_raw + b_raw;  // multiple of 1024
-    static constexpr int USTAGES = packed ? 2 : 0;
-    static constexpr int a_unp = APK ? BM * BK : 0;
-    static constexpr int b_unp = BPK ? BN * BK : 0;
-    static constexpr int unp_stage = a_unp + b_unp;
-    static constexpr int unp_off = STAGES * raw_stage;
-    static constexpr int bar_off = unp_off + USTAGES * unp_stage;
-    static constexpr int n_bars = 2 * STAGES + 2 * USTAGES + 4;
-    static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;  // + alignment slack
-    static constexpr int unpack_warps = packed ? 8 : 0;
-    static constexpr int threads = 256 + 32 * unpack_warps;
-    // Arrivals that free a raw stage: the MMA commit if it reads an int8
-    // operand straight from the raw stage, plus one per unpack warp.
-    // Unpack warps form two teams that take alternate k-blocks (two stages in
-    // flight); a stage is read by one team.
-    static constexpr int team_warps = unpack_warps / 2;
-    static constexpr int raw_release = (APK && BPK ? 0 : 1) + team_warps;
-};
-
-// FQG_I4 layout: per group of 32 k, byte i (0..15) = q[i] & 15 | q[16 + i] << 4.
-// 16 packed bytes -> the group's 32 int8: low nibbles are k 0..15 in order,
-// high nibbles k 16..31. Per nibble v: ((v ^ 8) + 0x78) ^ 0x80 is v
-// sign-extended to 8 bits with no carry between byte lanes ((v ^ 8) + 0x78
-// <= 0x87); the AND and first XOR fuse into one LOP3.
-__device__ __forceinline__ uint32_t sext4x4(uint32_t nib) {
-    return ((nib ^ 0x08080808u) + 0x78787878u) ^ 0x80808080u;
-}
-__device__ __forceinline__ void unpack16(uint4 p, uint4& o0, uint4& o1) {
-    o0 = make_uint4(sext4x4(p.x & 0x0F0F0F0Fu), sext4x4(p.y & 0x0F0F0F0Fu),
-                    sext4x4(p.z & 0x0F0F0F0Fu), sext4x4(p.w & 0x0F0F0F0Fu));
-    o1 = make_uint4(sext4x4((p.x >> 4) & 0x0F0F0F0Fu), sext4x4((p.y >> 4) & 0x0F0F0F0Fu),
-                    sext4x4((p.z >> 4) & 0x0F0F0F0Fu), sext4x4((p.w >> 4) & 0x0F0F0F0Fu));
-}
-
-// Biased nibbles u = q + 8 in [0, 15] -> unsigned bytes: one AND (low) and
-// SHIFT + AND (high) per 4 values.
-__device__ __forceinline__ void unpack16_biased(uint4 p, uint4& o0, uint4& o1) {
-    o0 = make_uint4(p.x & 0x0F0F0F0Fu, p.y & 0x0F0F0F0Fu, p.z & 0x0F0F0F0Fu, p.w & 0x0F0F0F0Fu);
-    o1 = make_uint4((p.x >> 4) & 0x0F0F0F0Fu, (p.y >> 4) & 0x0F0F0F0Fu, (p.z >> 4) & 0x0F0F0F0Fu,
-                    (p.w >> 4) & 0x0F0F0F0Fu);
-}
-
-__device__ __forceinline__ uint4 lds128(uint32_t addr) {
-    uint4 v;
-    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "r"(addr));
-    return v;
-}
-__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
-    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y),
-                 "r"(v.z), "r"(v.w)
-                 : "memory");
-}
-
-// Expand `rows` x 64 packed bytes (plain rows) into rows x 128 int8 in the
-// 128B-swizzle K-major layout: 16-byte chunk c of row r at r*128 + ((c ^ r%8) * 16).
-// Shared-window 32-bit addresses (ld/st.shared), so no generic-address math.
-template <int FMT>
-__device__ __forceinline__ void unpack_tile(const uint8_t* src, uint8_t* dst, int rows, int tid,
-                                            int nthreads) {
-    const uint32_t s0 = ptx::smem_u32(src), d0 = ptx::smem_u32(dst);
-#pragma unroll 4
-    for (int u = tid; u < rows * 4; u += nthreads) {
-        const int r = u >> 2, pc = u & 3;
-        const uint4 p = lds128(s0 + static_cast<uint32_t>(u) * 16);  // == r * 64 + pc * 16
-        uint4 o0, o1;
-        if constexpr (FMT == FU4)
-            unpack16_biased(p, o0, o1);
-        else
-            unpack16(p, o0, o1);
-        const uint32_t row = d0 + static_cast<uint32_t>(r) * 128;
-        const int sw = r & 7;
-        sts128(row + (((2 * pc) ^ sw) << 4), o0);
-        sts128(row + (((2 * pc + 1) ^ sw) << 4), o1);
-    }
-}
-
-__device__ __forceinline__ double load_bias(const void* bias, int dt, int col) {
-    switch (dt) {
-        case FQG_F32: return static_cast<double>(static_cast<const float*>(bias)[col]);
-        case FQG_F64: return static_cast<const double*>(bias)[col];
-        case FQG_F16: return static_cast<double>(__half2float(static_cast<const __half*>(bias)[col]));
-        case FQG_BF16:
-            return static_cast<double>(__bfloat162float(static_cast<const __nv_bfloat16*>(bias)[col]));
-        default: return 0.0;
-    }
-}
-
-template <int OUT>
-__device__ __forceinline__ void store_one(void* y, int64_t idx, int32_t acc, double s, double b) {
-    if constexpr (OUT == FQG_I32) {
-        static_cast<int32_t*>(y)[idx] = acc;
-    } else {
-        // quantize.cpp:196: out = double(acc) * (s_x * s_w); + bias extension.
-        const double v = static_cast<double>(acc) * s + b;
-        if constexpr (OUT == FQG_F64) static_cast<double*>(y)[idx] = v;
-        if constexpr (OUT == FQG_F32) static_cast<float*>(y)[idx] = static_cast<float>(v);
-        if constexpr (OUT == FQG_F16) static_cast<__half*>(y)[idx] = __double2half(v);
-        if constexpr (OUT == FQG_BF16) static_cast<__nv_bfloat16*>(y)[idx] = __double2bfloat16(v);
-    }
-}
-
-// 32 consecutive columns of one row, from 32 accumulator registers.
-template <int OUT>
-__device__ __forceinline__ void store_row_chunk(void* y, int64_t base, uint32_t (&r)[32],
-                                                double s, const void* bias, int bias_dt, int col0,
-                                                int ncols, bool vec, int32_t corr) {
-    if (corr != 0) {
-#pragma unroll
-        for (int c = 0; c < 32; ++c) r[c] = static_cast<uint32_t>(static_cast<int32_t>(r[c]) - corr);
-    }
-    if (vec && ncols == 32) {
-        if constexpr (OUT == FQG_I32) {
-            int4* p = reinterpret_cast<int4*>(static_cast<int32_t*>(y) + base);
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                p[q] = make_int4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-            return;
-        } else if constexpr (OUT == FQG_F16 || OUT == FQG_BF16) {
-            uint32_t packed[16];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) {
-                double v0 = static_cast<double>(static_cast<int32_t>(r[2 * q])) * s;
-                double v1 = static_cast<double>(static_cast<int32_t>(r[2 * q + 1])) * s;
-                if (bias) {
-                    v0 += load_bias(bias, bias_dt, col0 + 2 * q);
-                    v1 += load_bias(bias, bias_dt, col0 + 2 * q + 1);
-                }
-                if constexpr (OUT == FQG_F16) {
-                    __half2 h = __halves2half2(__double2half(v0), __double2half(v1));
-                    packed[q] = *reinterpret_cast<uint32_t*>(&h);
-                } else {
-                    __nv_bfloat162 h;
-                    h.x = __double2bfloat16(v0);
-                    h.y = __double2bfloat16(v1);
-                    packed[q] = *reinterpret_cast<uint32_t*>(&h);
-                }
-            }
-            uint4* p = reinterpret_cast<uint4*>(static_cast<uint16_t*>(y) + base);
-#pragma unroll
-            for (int q = 0; q < 4; ++q)  // streaming stores: the output is not re-read here
-                __stcs(p + q, make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2],
-                                         packed[4 * q + 3]));
-            return;
-        }
-    }
-#pragma unroll
-    for (int c = 0; c < 32; ++c) {
-        if (c < ncols) {
-            const double b = bias ? load_bias(bias, bias_dt, col0 + c) : 0.0;
-            store_one<OUT>(y, base + c, static_cast<int32_t>(r[c]), s, b);
-        }
-    }
-}
-
-template <int OUT>
-struct OutT;
-template <> struct OutT<FQG_I32> { using T = int32_t; };
-template <> struct OutT<FQG_F64> { using T = double; };
-template <> struct OutT<FQG_F32> { using T = float; };
-template <> struct OutT<FQG_F16> { using T = __half; };
-template <> struct OutT<FQG_BF16> { using T = __nv_bfloat16; };
-
-template <int OUT>
-__device__ __forceinline__ typename OutT<OUT>::T convert_out(int32_t acc, double s, double b) {
-    if constexpr (OUT == FQG_I32) {
-        return acc;
-    } else {
-        const double v = static_cast<double>(acc) * s + b;  // quantize.cpp:196 (+ bias)
-        if constexpr (OUT == FQG_F64) return v;
-        if constexpr (OUT == FQG_F32) return static_cast<float>(v);
-        if constexpr (OUT == FQG_F16) return __double2half(v);
-        if constexpr (OUT == FQG_BF16) return __double2bfloat16(v);
-    }
-}
-
-template <int BN, int STAGES, int OUT, int AF, int BF>
-__global__ void __launch_bounds__(Layout<BN, STAGES, AF != F8, BF != F8>::threads, 1)
-    k_gemm_i8(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
-              const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
-              int vec_ok, const int32_t* __restrict__ rowsum) {
-    constexpr bool APK = AF != F8, BPK = BF != F8;
-    using L = Layout<BN, STAGES, APK, BPK>;
-    constexpr int U = L::USTAGES;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);
-    uint64_t* empty = full + STAGES;
-    uint64_t* ufull = empty + STAGES;   // [U] unpacked stage ready
-    uint64_t* uempty = ufull + U;       // [U] unpacked stage consumed by the MMA
-    uint64_t* tfull = uempty + U;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int num_m = (m + BM - 1) / BM;
-    const int num_n = (n + BN - 1) / BN;
-    const int num_tiles = num_m * num_n;
-
-    if (threadIdx.x == 0) {
-        ptx::tma_prefetch_desc(&tmA);
-        ptx::tma_prefetch_desc(&tmB);
-        for (int s = 0; s < STAGES; ++s) {
-            ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&empty[s], L::raw_release);
-        }
-        for (int u = 0; u < U; ++u) {
-            ptx::mbar_init(&ufull[u], L::team_warps);
-            ptx::mbar_init(&uempty[u], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 4);
-        }
-        ptx::fence_barrier_init();
-    }
-    if (warp == 1) {
-        ptx::tmem_alloc(tmem_holder, 2 * BN);
-        ptx::tmem_relinquish();
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
-
-    if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer ----------------
-        const uint64_t keep = ptx::policy_evict_last();
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int m_blk = tile % num_m, n_blk = tile / num_m;
-            for (int kb = 0; kb < num_kb; ++kb) {
-                ptx::mbar_wait(&empty[stage], phase ^ 1);
-                uint8_t* sa = smem + stage * L::raw_stage;
-                uint8_t* sb = sa + L::a_raw;
-                ptx::mbar_arrive_expect_tx(&full[stage], L::raw_stage);
-                ptx::tma_load_2d_hint(sa, &tmA, &full[stage], kb * (APK ? BK / 2 : BK), m_blk * BM,
-                                      keep);
-                ptx::tma_load_2d_hint(sb, &tmB, &full[stage], kb * (BPK ? BK / 2 : BK), n_blk * BN,
-                                      keep);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    } else if (warp == 1 && lane == 0) {
-        // ---------------- MMA issuer ----------------
-        constexpr uint32_t idesc = ptx::idesc_i8(BM, BN, BF == FU4);
-        int stage = 0, us = 0;
-        uint32_t phase = 0, uphase = 0;
-        int it = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            ptx::mbar_wait(&tempty[acc], acc_phase ^ 1);
-            ptx::tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < num_kb; ++kb) {
-                ptx::mbar_wait(&full[stage], phase);
-                if constexpr (L::packed) ptx::mbar_wait(&ufull[us], uphase);
-                ptx::tc_fence_after();
-                const uint32_t raw = ptx::smem_u32(smem + stage * L::raw_stage);
-                const uint32_t unp = ptx::smem_u32(smem + L::unp_off + us * L::unp_stage);
-                const uint32_t a_addr = APK ? unp : raw;
-                const uint32_t b_addr = BPK ? unp + L::a_unp : raw + L::a_raw;
-#pragma unroll
-                for (int k = 0; k < BK / UK; ++k) {
-                    ptx::mma_i8(d_tmem, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
-                                ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
-                                (kb | k) != 0 ? 1u : 0u);
-                }
-                if constexpr (!(APK && BPK)) ptx::mma_commit(&empty[stage]);
-                if constexpr (L::packed) {
-                    ptx::mma_commit(&uempty[us]);
-                    if (++us == U) {
-                        us = 0;
-                        uphase ^= 1;
-                    }
-                }
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-            ptx::mma_commit(&tfull[acc]);
-        }
-    } else if (warp >= 4 && warp < 8) {
-        // ---------------- epilogue ----------------
-        const int ew = warp - 4;  // TMEM lane quarter this warp may access
-        // quantize.cpp:193: the product s_x * s_w formed once in FP64.
-        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
-        int it = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-            const int m_blk = tile % num_m, n_blk = tile / num_m;
-            const int acc = it & 1;
-            const uint32_t acc_phase = (it >> 1) & 1;
-            ptx::mbar_wait(&tfull[acc], acc_phase);
-            ptx::tc_fence_after();
-            const int row = m_blk * BM + ew * 32 + lane;
-            const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
-                ptx::tmem_wait_ld();
-                const int col0 = n_blk * BN + c * 32;
-                if (row < m && col0 < n) {
-                    const int ncols = min(32, n - col0);
-                    store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
-                                         bias_dt, col0, ncols, vec_ok != 0, corr);
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-        }
-    } else if (L::packed && warp >= 8) {
-        // ---------------- int4 -> int8 unpack warps ----------------
-        const int team = (warp - 8) / L::team_warps;
-        const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
-        int stage = 0, us = 0, step = 0;
-        uint32_t phase = 0, uphase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            for (int kb = 0; kb < num_kb; ++kb, ++step) {
-                if ((step & 1) != team) {
-                    if (++us == U) {
-                        us = 0;
-                        uphase ^= 1;
-                    }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                    continue;
-                }
-                ptx::mbar_wait(&full[stage], phase);
-                ptx::mbar_wait(&uempty[us], uphase ^ 1);
-                const uint8_t* raw = smem + stage * L::raw_stage;
-                uint8_t* unp = smem + L::unp_off + us * L::unp_stage;
-                if constexpr (APK) unpack_tile<AF>(raw, unp, BM, utid, nut);
-                if constexpr (BPK) unpack_tile<BF>(raw + L::a_raw, unp + L::a_unp, BN, utid, nut);
-                // generic-proxy smem writes -> visible to the tensor core (async proxy)
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive(&ufull[us]);
-                    ptx::mbar_arrive(&empty[stage]);
-                }
-                if (++us == U) {
-                    us = 0;
-                    uphase ^= 1;
-                }
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    }
-    __syncthreads();
-    if (warp == 1) {
-        __syncwarp();
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 2 * BN);
-    }
-}
-
-// Developer instrumentation (FQG_GEMM_DEBUG=1): per-CTA cycles spent in each
-// role's barrier waits. Off by default (one predicated branch per wait).
-__device__ unsigned long long g_dbg[296][8];
-__device__ unsigned long long g_dbg2[296][8];  // pair packed path: see launch_pair
-#define FQG_TWAIT2(slot, ...)                                                  \
-    do {                                                                       \
-        const long long t0_ = dbg ? clock64() : 0;                             \
-        __VA_ARGS__;                                                           \
-        if (dbg) atomicAdd(&g_dbg2[blockIdx.x % 296][slot], clock64() - t0_);  \
-    } while (0)
-#define FQG_TWAIT(slot, ...)                                                   \
-    do {                                                                       \
-        const long long t0_ = dbg ? clock64() : 0;                             \
-        __VA_ARGS__;                                                           \
-        if (dbg) atomicAdd(&g_dbg[blockIdx.x % 296][slot], clock64() - t0_);   \
-    } while (0)
-
-// ------------------------------------------------------------------------
-// CTA-pair variant (cta_group::2): a cluster of 2 CTAs on one TPC computes a
-// 256 x 256 output tile with tcgen05.mma.cta_group::2 (M = 256, N = 256,
-// K = 32). Each CTA stages its own 128 rows of A and 128 of the 256 rows of
-// B, so per SM the smem/L2 operand traffic per MMA drops from 48 KB to 32 KB
-// per 128-deep k-block versus the 1-CTA 128 x 256 tile. The even CTA issues
-// the MMAs; commits multicast to both CTAs' barriers; each CTA's epilogue
-// drains its own TMEM half (its 128 rows x 256 columns).
-//   int8 operands: 2-SM TMA (completion counted on the leader's barrier);
-//   packed int4 operands: 1-SM TMA into this CTA's raw ring, local unpack
-//   warps expand to int8 and signal the leader.
-// NB = 256-column blocks of B per tile: NB = 1 -> 256 x 256 tiles with a
-// double-buffered accumulator; NB = 2 -> 256 x 512 tiles, two accumulators
-// filling TMEM (no double buffer): the A tile is read once per two MMAs, so
-// L2 -> SMEM bytes per MAC drop by a quarter (the kernel is TMA-throughput bound).
-template <int STAGES, bool APK, bool BPK, int NB = 1, int EPIB = 0>
-struct PairLayout {
-    static constexpr int BN = 256;
-    static constexpr int NACC = NB == 1 ? 2 : 1;  // accumulator buffers
-    static constexpr bool packed = APK || BPK;
-    static constexpr int a_raw = APK ? BM * BK / 2 : BM * BK;       // own 128 rows of A
-    static constexpr int b_raw = NB * (BPK ? (BN / 2) * BK / 2 : (BN / 2) * BK);  // own halves of B
-    static constexpr int raw_stage = a_raw + b_raw;
-    static constexpr int direct_bytes = (APK ? 0 : a_raw) + (BPK ? 0 : b_raw);
-    static constexpr int packed_bytes = (APK ? a_raw : 0) + (BPK ? b_raw : 0);
-    static constexpr int USTAGES = packed ? (NB == 1 ? 4 : 3) : 0;
-    static constexpr int a_unp = APK ? BM * BK : 0;
-    static constexpr int b_unp = BPK ? NB * (BN / 2) * BK : 0;
-    static constexpr int unp_stage = a_unp + b_unp;
-    static constexpr int unp_off = STAGES * raw_stage;
-    // epilogue staging: per epilogue warp 2 buffers of a 32 x 32 output block
-    // (the box of a TMA tensor store); EPIB = bytes of one block, 0 = direct stores
-    static constexpr int epi_off = unp_off + USTAGES * unp_stage;
-    static constexpr int bar_off = epi_off + 4 * 2 * EPIB;
-    static constexpr int n_bars = 3 * STAGES + 2 * USTAGES + 4;
-    static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
-    static constexpr int unpack_warps = packed ? 8 : 0;
-    // epilogue warp groups (4 warps each): NB = 2 drains its single accumulator
-    // after the main loop with the unpack warps (or 4 spare warps) joining in
-    // (4-byte outputs keep one group and the staged TMA-store epilogue instead)
-    static constexpr int epi_groups = (NB == 2 && EPIB != 32 * 32 * 4) ? (packed ? 3 : 4) : 1;
-    // spare warps (after the unpack warps, if any) that only run epilogue groups
-    static constexpr int spare_warps = (epi_groups - 1) * 4 - (packed && epi_groups > 1 ? unpack_warps : 0);
-    static constexpr int threads = 256 + 32 * (unpack_warps + spare_warps);
-    static constexpr int tmem_cols = NB == 1 ? 2 * BN : NB * BN;
-    // Arrivals freeing a raw stage in each CTA: the leader's multicast MMA
-    // commit when an operand is read straight from the raw stage, plus one per
-    // local unpack warp that reads it.
-    static constexpr int team_warps = unpack_warps / 2;  // alternate k-blocks, as in Layout
-    static constexpr int raw_release = (direct_bytes > 0 ? 1 : 0) + (packed_bytes > 0 ? team_warps : 0);
-    static_assert(tmem_cols <= 512, "TMEM budget");
-};
-
-// Staged TMA-store epilogue for 4-byte outputs (f32 at 2048x4096: 97 -> 71 us);
-// 2-byte outputs keep direct 16-byte stores (measured faster: 60 vs 66 us),
-// f64 keeps direct stores (the staging would not fit next to the rings).
-template <int OUT>
-constexpr int epi_block_bytes() {
-    return (OUT == FQG_F32 || OUT == FQG_I32) ? 32 * 32 * 4 : 0;
-}
-
-template <int STAGES, int OUT, int AF, int BF, int NB>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
-    PairLayout<STAGES, AF != F8, BF != F8, NB, epi_block_bytes<OUT>()>::threads, 1)
-    k_gemm_i8_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   void* __restrict__ y, int64_t ldy, int m, int n, int num_kb,
-                   const double* __restrict__ scale, const void* __restrict__ bias, int bias_dt,
-                   int vec_ok, int dbg, const int32_t* __restrict__ rowsum, int sk,
-                   int32_t* __restrict__ ws, int* __restrict__ ws_flag,
-                   const __grid_constant__ CUtensorMap tmY, int tma_y) {
-    constexpr bool APK = AF != F8, BPK = BF != F8;
-    constexpr int EPIB = epi_block_bytes<OUT>();
-    using L = PairLayout<STAGES, APK, BPK, NB, EPIB>;
-    using OT = typename OutT<OUT>::T;
-    constexpr int NACC = L::NACC;
-    constexpr int NG = L::epi_groups;
-    constexpr int TN = NB * L::BN;  // tile columns
-    const long long t_start = clock64();
-    unsigned long long gstart = 0;
-    if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gstart));
-    constexpr int BN = L::BN;
-    constexpr int U = L::USTAGES;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* full_mma = reinterpret_cast<uint64_t*>(smem + L::bar_off);  // leader: direct operands
-    uint64_t* full_unp = full_mma + STAGES;  // own: packed operands landed
-    uint64_t* empty = full_unp + STAGES;     // own: raw stage free
-    uint64_t* ufull = empty + STAGES;        // leader: unpacked stage ready (both CTAs)
-    uint64_t* uempty = ufull + U;            // own: unpacked stage consumed
-    uint64_t* tfull = uempty + U;            // own: accumulator ready
-    uint64_t* tempty = tfull + 2;            // leader: accumulator drained (both CTAs)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = ptx::cluster_ctarank();
-    const bool leader = rank == 0;
-    const int num_m = (m + 2 * BM - 1) / (2 * BM);
-    const int num_n = (n + TN - 1) / TN;
-    const int num_tiles = num_m * num_n;
-    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    // Work of this cluster as segments (tile, kb0, kb1, wslot, fslot, nf).
-    //  sk == 0: data-parallel, whole tiles round robin.
-    //  sk == 1: stream-K: the tile x k-block units are cut into ncl equal
-    //    contiguous ranges (each >= one tile, so a tile is split at most two
-    //    ways): a range that starts inside a tile leaves its partial INT32 sums
-    //    in ws[cid] (flag += 8 warps); the owner of the tile's head adds
-    //    ws[cid + 1] in its epilogue.
-    //  sk >= 2: split-K by sk (small M): unit u = cid is split s = u % sk of
-    //    tile u / sk; every split writes its raw INT32 partial to the full-size
-    //    plane ws[s][M][N] (wslot = -2 - s) and k_splitk_reduce sums the planes
-    //    and runs the epilogue.
-    // Integer partial sums: exact and order-free.
-    // Split modes only exist in the NB = 1 instantiation (small-M and ragged
-    // tile counts); the 256 x 512 kernel keeps the plain data-parallel loop.
-    constexpr bool SPLITS = NB == 1;
-    auto for_each_seg = [&](auto&& f) {
-        if (!SPLITS || sk == 0) {
-            for (int tile = cid; tile < num_tiles; tile += ncl) f(tile, 0, num_kb, -1, 0, 0);
-        } else if (sk == 1) {
-            const int64_t total = static_cast<int64_t>(num_tiles) * num_kb;
-            const int u0 = static_cast<int>(total * cid / ncl);
-            const int u1 = static_cast<int>(total * (cid + 1) / ncl);
-            for (int u = u0; u < u1;) {
-                const int tile = u / num_kb, kb0 = u % num_kb;
-                const int kb1 = min(num_kb, kb0 + (u1 - u));
-                f(tile, kb0, kb1, kb0 > 0 ? cid : -1, cid + 1, kb1 < num_kb ? 1 : 0);
-                u += kb1 - kb0;
-            }
-        } else if (sk >= 2) {
-            if (cid < num_tiles * sk) {
-                const int tile = cid / sk, sp = cid % sk;
-                const int kb0 = sp * num_kb / sk, kb1 = (sp + 1) * num_kb / sk;
-                f(tile, kb0, kb1, -2 - sp, 0, 0);
-            }
-        } else {
-            for (int tile = cid; tile < num_tiles; tile += ncl) f(tile, 0, num_kb, -1, 0, 0);
-        }
-    };
-
-    if (threadIdx.x == 0) {
-        ptx::tma_prefetch_desc(&tmA);
-        ptx::tma_prefetch_desc(&tmB);
-        for (int s = 0; s < STAGES; ++s) {
-            ptx::mbar_init(&full_mma[s], 1);
-            ptx::mbar_init(&full_unp[s], 1);
-            ptx::mbar_init(&empty[s], L::raw_release);
-        }
-        for (int u = 0; u < U; ++u) {
-            ptx::mbar_init(&ufull[u], 2 * L::team_warps);  // one team's warps in both CTAs
-            ptx::mbar_init(&uempty[u], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 8 * (L::packed ? 1 : NG));
-        }
-        ptx::fence_barrier_init();
-    }
-    if (warp == 1) {
-        ptx::tmem_alloc_pair(tmem_holder, L::tmem_cols);
-        ptx::tmem_relinquish_pair();
-    }
-    ptx::tc_fence_before();
-    ptx::cluster_sync();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
-    // Launched as a programmatic dependent of K1: everything above overlapped
-    // K1's tail; A, the row sums and y are touched only after this.
-    ptx::griddep_wait();
-
-    // ---------------- epilogue (both CTAs: own 128 rows) ----------------
-    // Lane quarter ew of TMEM; group grp of NG takes chunks grp, grp + NG, ...
-    // (with one accumulator, NB = 2, the unpack warps / spare warps join after
-    // the main loop so the exposed drain is split NG ways).
-    // Helpers (grp > 0): with packed operands the unpack warps only reach the
-    // epilogue after their whole loop, so they help on the cluster's LAST tile
-    // and never arrive on tempty (nothing reuses the accumulator after it);
-    // spare warps (int8 operands) help on every tile and arrive.
-    constexpr bool HELP_ALL = !L::packed;
-    auto run_epilogue = [&](const int ew, const int grp) {
-        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
-        int it = 0, echunk = 0;
-        if (EPIB > 0 && tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
-        for_each_seg([&](int tile, int, int, int wslot, int fslot, int nf) {
-            const bool last = tile + ncl >= num_tiles || (SPLITS && sk != 0);
-            const int ng = (HELP_ALL || last) ? NG : 1;  // groups sharing this tile's chunks
-            if (grp >= ng) {  // a helper skips this tile (keeps the phase count)
-                // Spare warps are idle, so they must observe every tfull phase in
-                // order (a parity wait two phases ahead would alias); the unpack
-                // warps only get here after all earlier phases completed.
-                if (warp >= 8 + L::unpack_warps) ptx::mbar_wait(&tfull[it % NACC], (it / NACC) & 1);
-                ++it;
-                return;
-            }
-            const int m_blk = tile % num_m, n_blk = tile / num_m;
-            const int acc = it % NACC;
-            const uint32_t acc_phase = (it / NACC) & 1;
-            const bool tail = SPLITS && wslot >= 0;    // partial sums -> ws[wslot]
-            const bool head = SPLITS && nf > 0;        // add ws[fslot .. fslot + nf)
-            const bool plane = SPLITS && wslot <= -2;  // split-K: raw partial -> plane -2 - wslot
-            ptx::mbar_wait(&tfull[acc], acc_phase);
-            ptx::tc_fence_after();
-            unsigned long long ge0 = 0;
-            if (dbg && lane == 0 && ew == 0 && grp == 0) {
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
-                atomicAdd(&g_dbg2[blockIdx.x % 296][6], ge0 - gstart);  // tfull reached (ns)
-            }
-            const int rloc = rank * BM + ew * 32 + lane;  // row within the 256-row tile
-            const int row = m_blk * 2 * BM + rloc;
-            const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-            if (head) {
-                if (lane == 0) {
-                    const long long tw0 = clock64();
-                    for (int f = 0; f < nf; ++f) {
-                        int v;
-                        do {
-                            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];"
-                                         : "=r"(v)
-                                         : "l"(ws_flag + fslot + f));
-                        } while (v < 8);
-                    }
-                    (void)tw0;
-                }
-                __syncwarp();
-            }
-#pragma unroll 1
-            for (int c = grp; c < TN / 32; c += ng) {
-                uint32_t r[32];
-                if (!(dbg & 8)) {
-                    ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
-                    ptx::tmem_wait_ld();
-                } else {
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) r[e] = static_cast<uint32_t>(c + e);
-                }
-                if (plane) {
-                    const int col0 = n_blk * TN + c * 32;
-                    if (row < m && col0 < n) {
-                        int32_t* dst = ws + (static_cast<int64_t>(-2 - wslot) * m + row) * n + col0;
-                        if (col0 + 32 <= n && (n & 3) == 0) {
-#pragma unroll
-                            for (int v = 0; v < 8; ++v)
-                                reinterpret_cast<int4*>(dst)[v] =
-                                    make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (col0 + e < n) dst[e] = static_cast<int32_t>(r[e]);
-                        }
-                    }
-                    continue;
-                }
-                if (tail) {
-                    // slot layout [chunk][v][256 rows][4]: each store instruction of a warp
-                    // writes 512 contiguous bytes
-                    int4* wp = reinterpret_cast<int4*>(ws + static_cast<int64_t>(wslot) * 256 * TN) +
-                               c * 8 * 256 + rloc;
-#pragma unroll
-                    for (int v = 0; v < 8; ++v)
-                        wp[v * 256] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-                    continue;
-                }
-                for (int f = 0; head && f < nf; ++f) {
-                    const int4* wp =
-                        reinterpret_cast<const int4*>(ws + static_cast<int64_t>(fslot + f) * 256 * TN) +
-                        c * 8 * 256 + rloc;
-#pragma unroll
-                    for (int v = 0; v < 8; ++v) {
-                        const int4 pv = __ldcg(wp + v * 256);
-                        r[4 * v] += pv.x, r[4 * v + 1] += pv.y, r[4 * v + 2] += pv.z, r[4 * v + 3] += pv.w;
-                    }
-                }
-                const int col0 = n_blk * TN + c * 32;
-                if constexpr (EPIB > 0) {
-                    if (tma_y) {  // convert, stage the 32 x 32 block, one TMA tensor store
-                        uint8_t* ep = smem + L::epi_off + (ew * 2 + (echunk & 1)) * EPIB;
-                        ++echunk;
-                        if (lane == 0) ptx::bulk_wait_read_allbut1();
-                        __syncwarp();
-                        constexpr int ESZ = static_cast<int>(sizeof(OT));
-                        uint32_t wv[32 * ESZ / 4];
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) {
-                            const double bv =
-                                bias != nullptr ? load_bias(bias, bias_dt, min(col0 + e, n - 1)) : 0.0;
-                            const OT v = convert_out<OUT>(static_cast<int32_t>(r[e]) - corr, s, bv);
-                            if constexpr (ESZ == 4) {
-                                wv[e] = *reinterpret_cast<const uint32_t*>(&v);
-                            } else {
-                                const uint32_t h = *reinterpret_cast<const uint16_t*>(&v);
-                                wv[e >> 1] = (e & 1) ? (wv[e >> 1] | (h << 16)) : h;
-                            }
-                        }
-                        uint4* dst = reinterpret_cast<uint4*>(ep + lane * 32 * ESZ);
-#pragma unroll
-                        for (int v = 0; v < 8 * ESZ / 4; ++v)
-                            dst[v] = make_uint4(wv[4 * v], wv[4 * v + 1], wv[4 * v + 2], wv[4 * v + 3]);
-                        ptx::fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) {
-                            ptx::tma_store_2d(&tmY, ep, col0, m_blk * 2 * BM + rank * BM + ew * 32);
-                            ptx::bulk_commit();
-                        }
-                        continue;
-                    }
-                }
-                if (row < m && col0 < n && !(dbg & 4)) {
-                    const int ncols = min(32, n - col0);
-                    store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
-                                         bias_dt, col0, ncols, vec_ok != 0, corr);
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0 && (HELP_ALL || grp == 0))
-                ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
-            if (tail) {  // publish the partial: release at gpu scope, one arrival per warp
-                __threadfence();
-                __syncwarp();
-                if (lane == 0) atomicAdd(ws_flag + wslot, 1);
-            }
-            if (dbg && lane == 0 && ew == 0 && grp == 0) {
-                unsigned long long ge1;
-                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge1));
-                atomicAdd(&g_dbg[blockIdx.x % 296][1], ge1 - ge0);
-                atomicAdd(&g_dbg[blockIdx.x % 296][2], 1ull);
-                atomicAdd(&g_dbg2[blockIdx.x % 296][7], ge1 - gstart);  // epilogue done (ns)
-            }
-            ++it;
-        });
-        if (EPIB > 0 && tma_y && lane == 0) ptx::bulk_wait_all();  // staged output stores
-    };
-
-    if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer (both CTAs) ----------------
-        const uint64_t keep = ptx::policy_evict_last();
-        int stage = 0;
-        uint32_t phase = 0;
-        for_each_seg([&](int tile, int kb0, int kb1, int, int, int) {
-            const int m_blk = tile % num_m, n_blk = tile / num_m;
-            const int a_row = m_blk * 2 * BM + rank * BM;
-            const int b_row = n_blk * TN + rank * (BN / 2);  // + nb * BN per block
-            for (int kb = kb0; kb < kb1; ++kb) {
-                ptx::mbar_wait(&empty[stage], phase ^ 1);
-                uint8_t* sa = smem + stage * L::raw_stage;
-                uint8_t* sb = sa + L::a_raw;
-                const uint32_t lead_full = ptx::mapa(ptx::smem_u32(&full_mma[stage]), 0);
-                if constexpr (L::direct_bytes > 0) {
-                    if (leader) ptx::mbar_arrive_expect_tx(&full_mma[stage], 2 * L::direct_bytes);
-                }
-                if constexpr (L::packed_bytes > 0)
-                    ptx::mbar_arrive_expect_tx(&full_unp[stage], L::packed_bytes);
-                if constexpr (APK)
-                    ptx::tma_load_2d_hint(sa, &tmA, &full_unp[stage], kb * BK / 2, a_row, keep);
-                else
-                    ptx::tma_load_2d_2sm(sa, &tmA, lead_full, kb * BK, a_row, keep);
-#pragma unroll
-                for (int nb = 0; nb < NB; ++nb) {
-                    if constexpr (BPK)
-                        ptx::tma_load_2d_hint(sb + nb * (L::b_raw / NB), &tmB, &full_unp[stage],
-                                              kb * BK / 2, b_row + nb * BN, keep);
-                    else
-                        ptx::tma_load_2d_2sm(sb + nb * (L::b_raw / NB), &tmB, lead_full, kb * BK,
-                                             b_row + nb * BN, keep);
-                }
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        });
-    } else if (warp == 1 && lane == 0 && leader) {
-        // ---------------- MMA issuer (leader CTA) ----------------
-        constexpr uint32_t idesc = ptx::idesc_i8(2 * BM, BN, BF == FU4);
-        int stage = 0, us = 0;
-        uint32_t phase = 0, uphase = 0;
-        int it = 0;
-        const long long t_mma0 = clock64();
-        unsigned long long g0;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
-        long long nkb_done = 0;
-        for_each_seg([&](int, int kb0, int kb1, int, int, int) {
-            const int acc = it % NACC;
-            const uint32_t acc_phase = (it / NACC) & 1;
-            FQG_TWAIT(2, ptx::mbar_wait(&tempty[acc], acc_phase ^ 1));
-            ptx::tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = kb0; kb < kb1; ++kb) {
-                if constexpr (L::direct_bytes > 0) FQG_TWAIT2(1, ptx::mbar_wait(&full_mma[stage], phase));
-                if constexpr (L::packed) FQG_TWAIT2(0, ptx::mbar_wait(&ufull[us], uphase));
-                ptx::tc_fence_after();
-                const uint32_t raw = ptx::smem_u32(smem + stage * L::raw_stage);
-                const uint32_t unp = ptx::smem_u32(smem + L::unp_off + us * L::unp_stage);
-                const uint32_t a_addr = APK ? unp : raw;
-                const uint32_t b_addr = BPK ? unp + L::a_unp : raw + L::a_raw;
-#pragma unroll
-                for (int k = 0; k < BK / UK; ++k) {
-#pragma unroll
-                    for (int nb = 0; nb < NB; ++nb)
-                        ptx::mma_i8_pair(d_tmem + nb * BN, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
-                                         ptx::smem_desc_sw128_kmajor(b_addr + nb * ((BN / 2) * BK) + k * UK),
-                                         idesc, (kb != kb0 || k != 0) ? 1u : 0u);
-                }
-                if constexpr (L::direct_bytes > 0) ptx::mma_commit_pair(&empty[stage], 0x3);
-                if constexpr (L::packed) {
-                    ptx::mma_commit_pair(&uempty[us], 0x3);
-                    if (++us == U) {
-                        us = 0;
-                        uphase ^= 1;
-                    }
-                }
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-            ptx::mma_commit_pair(&tfull[acc], 0x3);
-            nkb_done += kb1 - kb0;
-            ++it;
-        });
-        if (dbg) {
-            atomicAdd(&g_dbg[blockIdx.x % 296][5], clock64() - t_mma0);
-            atomicAdd(&g_dbg[blockIdx.x % 296][6], static_cast<unsigned long long>(nkb_done));
-            atomicAdd(&g_dbg[blockIdx.x % 296][7], t_mma0 - t_start);
-            unsigned long long g1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g1));
-            atomicAdd(&g_dbg[blockIdx.x % 296][4], g1 - g0);  // ns of the MMA loop
-        }
-    } else if (warp >= 4 && warp < 8) {
-        run_epilogue(warp - 4, 0);
-    } else if (L::packed && warp >= 8 && warp < 8 + L::unpack_warps) {
-        // ---------------- int4 -> int8 unpack warps (both CTAs) ----------------
-        const int team = (warp - 8) / L::team_warps;
-        const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
-        int stage = 0, us = 0, step = 0;
-        uint32_t phase = 0, uphase = 0;
-        for_each_seg([&](int, int kb0, int kb1, int, int, int) {
-            for (int kb = kb0; kb < kb1; ++kb, ++step) {
-                if ((step & 1) != team) {
-                    if (++us == U) {
-                        us = 0;
-                        uphase ^= 1;
-                    }
-                    if (++stage == STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                    continue;
-                }
-                const bool d0 = dbg && utid == 0;
-                long long tw0 = d0 ? clock64() : 0;
-                ptx::mbar_wait(&full_unp[stage], phase);
-                long long tw1 = d0 ? clock64() : 0;
-                ptx::mbar_wait(&uempty[us], uphase ^ 1);
-                long long tw2 = d0 ? clock64() : 0;
-                const uint8_t* raw = smem + stage * L::raw_stage;
-                uint8_t* unp = smem + L::unp_off + us * L::unp_stage;
-                if constexpr (APK) unpack_tile<AF>(raw, unp, BM, utid, nut);
-                if constexpr (BPK)
-                    unpack_tile<BF>(raw + L::a_raw, unp + L::a_unp, NB * (BN / 2), utid, nut);
-                if (d0) {
-                    atomicAdd(&g_dbg2[blockIdx.x % 296][2], tw1 - tw0);
-                    atomicAdd(&g_dbg2[blockIdx.x % 296][3], tw2 - tw1);
-                    atomicAdd(&g_dbg2[blockIdx.x % 296][4], clock64() - tw2);
-                    atomicAdd(&g_dbg2[blockIdx.x % 296][5], 1ull);
-                }
-                ptx::fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&ufull[us]), 0));
-                    ptx::mbar_arrive(&empty[stage]);
-                }
-                if (++us == U) {
-                    us = 0;
-                    uphase ^= 1;
-                }
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        });
-        if constexpr (NG > 1) run_epilogue(warp & 3, 1 + (warp - 8) / 4);
-    } else if (NG > 1 && warp >= 8) {  // spare warps: epilogue groups only
-        run_epilogue(warp & 3, 1 + (warp - 8) / 4);
-    }
-    ptx::tc_fence_before();
-    ptx::cluster_sync();
-    if (warp == 1) {
-        __syncwarp();
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc_pair(tmem_base, L::tmem_cols);
-    }
-    if (dbg && threadIdx.x == 32) {
-        unsigned long long gend;
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gend));
-        g_dbg[blockIdx.x % 296][0] = gstart;
-        g_dbg[blockIdx.x % 296][3] = gend;
-    }
-}
-
-// ------------------------------------------------------------------------
-// Weights-in-TMEM kernel for biased int4 weights ("swap AB"): Y^T = W . X^T.
-// The 128 weight rows of a tile are the MMA's M side and live in TENSOR
-// memory: two teams of 4 unpack warps load the packed rows from L2 into
-// registers (64 bytes per lane per k-block), unpack the biased nibbles with
-// one AND per 4 values and tcgen05.st them into a 4-stage A ring in TMEM. The
-// activations (int8) are the N side: TMA -> 128B-swizzled SMEM ring. Shared
-// memory then only carries the activation tile (TMA write + MMA read), so the
-// int4 unpack no longer competes with the tensor core for SMEM bandwidth.
-// A is fed as UNSIGNED int8 (nibble = q + 8); the epilogue subtracts
-// 8 * rowsum(x_token) per output column (exact in int32).
-// TMEM: accumulators [0, 2 BN) (double-buffered), A stages [2 BN, 2 BN + 128).
-constexpr int kW4AStages = 4;
-template <int BN, int STAGES, int ESZ = 8>
-struct W4Layout {
-    static constexpr int b_stage = BN * BK;  // activation rows x 128 bytes
-    // epilogue transpose tiles: per warp 2 buffers of 32 tokens x 32 features
-    // (dense rows of 32 * ESZ bytes: the box a TMA tensor store writes)
-    static constexpr int epi_row = 32 * ESZ;
-    static constexpr int epi_buf = 32 * epi_row;
-    static constexpr int epi_off = STAGES * b_stage;
-    static constexpr int bar_off = epi_off + 4 * 2 * epi_buf;
-    static constexpr int n_bars = 2 * STAGES + 2 * kW4AStages + 4;
-    static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
-    static constexpr int threads = 512;
-    static constexpr uint32_t a_col0 = 2 * BN;
-    static_assert(2 * BN + 32 * kW4AStages <= 512, "TMEM budget");
-};
-
-template <int BN, int STAGES, int OUT>
-__global__ void __launch_bounds__(512, 1)
-    k_gemm_w4t(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w,
-               int64_t ldb, int kbytes, void* __restrict__ y, int64_t ldy, int m, int n,
-               int num_kb, const double* __restrict__ scale, const void* __restrict__ bias,
-               int bias_dt, const int32_t* __restrict__ rowsum, int vec_ok, int dbg,
-               const __grid_constant__ CUtensorMap tmY, int tma_y) {
-    using OT = typename OutT<OUT>::T;
-    constexpr int ESZ = sizeof(OT);
-    using L = W4Layout<BN, STAGES, ESZ>;
-    constexpr int AS = kW4AStages;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);
-    uint64_t* empty = full + STAGES;
-    uint64_t* afull = empty + STAGES;
-    uint64_t* aempty = afull + AS;
-    uint64_t* tfull = aempty + AS;
-    uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int num_t = (m + BN - 1) / BN, num_f = (n + 127) / 128;
-    const int num_tiles = num_t * num_f;
-    if (threadIdx.x == 0) {
-        ptx::tma_prefetch_desc(&tmX);
-        for (int i = 0; i < STAGES; ++i) {
-            ptx::mbar_init(&full[i], 1);
-            ptx::mbar_init(&empty[i], 1);
-        }
-        for (int i = 0; i < AS; ++i) {
-            ptx::mbar_init(&afull[i], 4);  // the 4 warps of the team that filled it
-            ptx::mbar_init(&aempty[i], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 4);
-        }
-        ptx::fence_barrier_init();
-    }
-    if (warp == 1) {
-        ptx::tmem_alloc(tmem_holder, 512);
-        ptx::tmem_relinquish();
-    }
-    ptx::tc_fence_before();
-    __syncthreads();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
-
-    if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer: activation tiles ----------------
-        const uint64_t keep = ptx::policy_evict_last();
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            const int t_blk = tile % num_t;
-            for (int kb = 0; kb < num_kb; ++kb) {
-                ptx::mbar_wait(&empty[stage], phase ^ 1);
-                ptx::mbar_arrive_expect_tx(&full[stage], L::b_stage);
-                ptx::tma_load_2d_hint(smem + stage * L::b_stage, &tmX, &full[stage], kb * BK,
-                                      t_blk * BN, keep);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    } else if (warp == 1 && lane == 0) {
-        // ---------------- MMA issuer: A (weights) from TMEM, B from SMEM ----------------
-        constexpr uint32_t idesc = ptx::idesc_i8(128, BN, /*b_unsigned=*/false, /*a_unsigned=*/true);
-        int stage = 0, as = 0, it = 0;
-        uint32_t phase = 0, aphase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-            const int acc = it & 1;
-            FQG_TWAIT2(0, ptx::mbar_wait(&tempty[acc], ((it >> 1) & 1) ^ 1));
-            ptx::tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < num_kb; ++kb) {
-                FQG_TWAIT2(1, ptx::mbar_wait(&full[stage], phase));
-                FQG_TWAIT2(2, ptx::mbar_wait(&afull[as], aphase));
-                ptx::tc_fence_after();
-                const uint32_t a_tmem = tmem_base + L::a_col0 + as * 32;
-                const uint32_t b_addr = ptx::smem_u32(smem + stage * L::b_stage);
-#pragma unroll
-                for (int k = 0; k < BK / UK; ++k)
-                    ptx::mma_i8_ts(d_tmem, a_tmem + k * (UK / 4),
-                                   ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
-                                   (kb | k) != 0 ? 1u : 0u);
-                ptx::mma_commit(&empty[stage]);
-                ptx::mma_commit(&aempty[as]);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-                if (++as == AS) {
-                    as = 0;
-                    aphase ^= 1;
-                }
-            }
-            ptx::mma_commit(&tfull[acc]);
-        }
-    } else if (warp >= 4 && warp < 8) {
-        // ---------------- epilogue: lane = weight row (feature), columns = tokens ----------------
-        // Each warp owns 32 features; per 32-token chunk it converts its column of
-        // accumulators, transposes them through shared memory and writes 32
-        // token rows of 32 consecutive features (32 * ESZ bytes each).
-        const int q = warp - 4;
-        uint8_t* const ep0 = smem + L::epi_off + q * 2 * L::epi_buf;
-        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);  // quantize.cpp:193
-        int it = 0, chunk = 0;
-        if (tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++it) {
-            const int f_blk = tile / num_t, t_blk = tile % num_t;
-            const int acc = it & 1;
-            if (lane == 0 && q == 0) {
-                FQG_TWAIT2(3, ptx::mbar_wait(&tfull[acc], (it >> 1) & 1));
-            }
-            __syncwarp();
-            ptx::mbar_wait(&tfull[acc], (it >> 1) & 1);
-            ptx::tc_fence_after();
-            const long long te0 = clock64();
-            const int f0 = f_blk * 128 + 32 * q, feat = f0 + lane;
-            const bool fok = feat < n;
-            const double bv = (bias != nullptr && fok) ? load_bias(bias, bias_dt, feat) : 0.0;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c, ++chunk) {
-                uint32_t r[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN + 32 * c,
-                                        r);
-                const int t0 = t_blk * BN + 32 * c;
-                const int rs = t0 + lane < m ? rowsum[t0 + lane] : 0;
-                uint8_t* ep = ep0 + (chunk & 1) * L::epi_buf;
-                if (tma_y) {  // this buffer's previous TMA store has read it
-                    if (lane == 0) ptx::bulk_wait_read_allbut1();
-                    __syncwarp();
-                }
-                ptx::tmem_wait_ld();
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {  // token j of the chunk -> row j of the tile
-                    const int corr = 8 * __shfl_sync(0xffffffffu, rs, j);
-                    *reinterpret_cast<OT*>(ep + j * L::epi_row + lane * ESZ) =
-                        convert_out<OUT>(static_cast<int32_t>(r[j]) - corr, s, bv);
-                }
-                if (tma_y) {
-                    ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0 && !(dbg & 4)) {
-                        ptx::tma_store_2d(&tmY, ep, f0, t0);
-                        ptx::bulk_commit();
-                    }
-                } else {
-                    __syncwarp();
-                    const int tok = t0 + lane;  // lane writes token row `lane`
-                    if (tok < m && !(dbg & 4)) {
-                        OT* dst = static_cast<OT*>(y) + static_cast<int64_t>(tok) * ldy + f0;
-                        for (int e = 0; e < 32 && f0 + e < n; ++e)
-                            dst[e] = *reinterpret_cast<const OT*>(ep + lane * L::epi_row + e * ESZ);
-                    }
-                    __syncwarp();
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
-            if (dbg && lane == 0 && q == 0) atomicAdd(&g_dbg2[blockIdx.x % 296][4], clock64() - te0);
-        }
-    } else if (warp >= 8) {
-        // ---------------- unpack teams: L2 -> registers -> TMEM A ring ----------------
-        // Team t takes steps t, t + 2, ... of the (tile, k-block) sequence; each
-        // lane keeps its weight row's next three steps (64 bytes each) in flight.
-        const int team = (warp - 8) >> 2, q = warp & 3;
-        const int my_tiles = blockIdx.x < num_tiles ? (num_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-        const int steps = my_tiles * num_kb;
-        auto load_step = [&](int st_i, uint4 (&v)[4]) {
-            if (st_i >= steps) return;
-            const int tile = blockIdx.x + (st_i / num_kb) * gridDim.x, kb = st_i % num_kb;
-            const int feat = (tile / num_t) * 128 + 32 * q + lane;
-            const uint8_t* wrow = w + static_cast<int64_t>(feat < n ? feat : 0) * ldb;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int off = kb * (BK / 2) + 16 * i;
-                v[i] = (feat < n && off < kbytes) ? __ldg(reinterpret_cast<const uint4*>(wrow + off))
-                                                  : make_uint4(0u, 0u, 0u, 0u);
-            }
-        };
-        auto process = [&](int st_i, const uint4 (&v)[4]) {
-            const int as = st_i % AS;
-            uint32_t wd[32];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t pw[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    wd[8 * i + e] = pw[e] & 0x0F0F0F0Fu;             // k = 32i + 4e .. +3
-                    wd[8 * i + 4 + e] = (pw[e] >> 4) & 0x0F0F0F0Fu;  // k = 32i + 16 + 4e ..
-                }
-            }
-            if (lane == 0 && q == 0) {
-                FQG_TWAIT2(5 + team, ptx::mbar_wait(&aempty[as], ((st_i / AS) & 1) ^ 1));
-            }
-            __syncwarp();
-            ptx::mbar_wait(&aempty[as], ((st_i / AS) & 1) ^ 1);
-            ptx::tc_fence_after();
-            if (!(dbg & 2))
-                ptx::tmem_st_32x32b_x32(
-                    tmem_base + (static_cast<uint32_t>(32 * q) << 16) + L::a_col0 + as * 32, wd);
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_relaxed(&afull[as]);
-        };
-        uint4 va[4], vb[4], vc[4];
-        load_step(team, va);
-        load_step(team + 2, vb);
-        load_step(team + 4, vc);
-        for (int st_i = team; st_i < steps; st_i += 6) {
-            process(st_i, va);
-            load_step(st_i + 6, va);
-            if (st_i + 2 >= steps) break;
-            process(st_i + 2, vb);
-            load_step(st_i + 8, vb);
-            if (st_i + 4 >= steps) break;
-            process(st_i + 4, vc);
-            load_step(st_i + 10, vc);
-        }
-    }
-    if (tma_y && warp >= 4 && warp < 8 && lane == 0) ptx::bulk_wait_all();  // epilogue stores
-    ptx::tc_fence_before();
-    __syncthreads();
-    if (warp == 1) {
-        __syncwarp();
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc(tmem_base, 512);
-    }
-}
-
-// ------------------------------------------------------------------------
-// CTA-pair weights-in-TMEM kernel (biased int4 weights): a cluster of 2 CTAs
-// computes a 256-feature x BN-token tile with tcgen05.mma.cta_group::2, A (the
-// weights, 128 rows per CTA) read from each CTA's TENSOR memory, B (the
-// activation tile, BN/2 token rows per CTA) from SMEM via 2-SM TMA. Each CTA's
-// unpack teams fill only their own TMEM (no cross-CTA data), arriving on the
-// leader's barrier; the epilogue (per CTA: its 128 features) transposes
-// through SMEM and leaves by TMA tensor stores.
-template <int BN, int STAGES, int ESZ, int NACC = 2>
-struct W4PairLayout {
-    static constexpr int b_half = (BN / 2) * BK;  // this CTA's token rows x 128 bytes
-    static constexpr int epi_row = 32 * ESZ;
-    static constexpr int epi_buf = 32 * epi_row;
-    static constexpr int epi_off = STAGES * b_half;
-    static constexpr int bar_off = epi_off + 4 * 2 * epi_buf;
-    static constexpr int n_bars = 2 * STAGES + 2 * kW4AStages + 4;
-    static constexpr int total = bar_off + n_bars * 8 + 16 + 1024;
-    static constexpr int threads = 512;
-    // NACC accumulators (2: the epilogue of tile i overlaps tile i + 1; 1: N = 256
-    // tokens, the largest and fastest MMA shape, epilogue drains before reuse)
-    static constexpr uint32_t a_col0 = NACC * BN;
-    static_assert(NACC * BN + 32 * kW4AStages <= 512, "TMEM budget");
-    static_assert(BN % 32 == 0 && (BN / 2) % 8 == 0, "token tile");
-};
-
-template <int BN, int STAGES, int OUT, int NACC>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1)
-    k_gemm_w4t_pair(const __grid_constant__ CUtensorMap tmX, const uint8_t* __restrict__ w,
-                    int64_t ldb, int kbytes, void* __restrict__ y, int64_t ldy, int m, int n,
-                    int num_kb, const double* __restrict__ scale, const void* __restrict__ bias,
-                    int bias_dt, const int32_t* __restrict__ rowsum,
-                    const __grid_constant__ CUtensorMap tmY, int tma_y, int dbg) {
-    const long long t_start = clock64();
-    using OT = typename OutT<OUT>::T;
-    constexpr int ESZ = sizeof(OT);
-    using L = W4PairLayout<BN, STAGES, ESZ, NACC>;
-    constexpr int AS = kW4AStages;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>(
-        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::bar_off);  // leader: both B halves
-    uint64_t* empty = full + STAGES;                                   // own: B stage free
-    uint64_t* afull = empty + STAGES;                                  // leader: A stage (both)
-    uint64_t* aempty = afull + AS;                                     // own: A stage free
-    uint64_t* tfull = aempty + AS;                                     // own: accumulator ready
-    uint64_t* tempty = tfull + 2;                                      // leader: drained (both)
-    uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = ptx::cluster_ctarank();
-    const bool leader = rank == 0;
-    const int num_t = (m + BN - 1) / BN, num_f = (n + 255) / 256;
-    const int num_tiles = num_t * num_f;
-    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
-    if (threadIdx.x == 0) {
-        ptx::tma_prefetch_desc(&tmX);
-        for (int i = 0; i < STAGES; ++i) {
-            ptx::mbar_init(&full[i], 1);
-            ptx::mbar_init(&empty[i], 1);
-        }
-        for (int i = 0; i < AS; ++i) {
-            ptx::mbar_init(&afull[i], 8);  // one team's 4 warps in both CTAs
-            ptx::mbar_init(&aempty[i], 1);
-        }
-        for (int a = 0; a < 2; ++a) {
-            ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 8);
-        }
-        ptx::fence_barrier_init();
-    }
-    if (warp == 1) {
-        ptx::tmem_alloc_pair(tmem_holder, 512);
-        ptx::tmem_relinquish_pair();
-    }
-    ptx::tc_fence_before();
-    ptx::cluster_sync();
-    ptx::tc_fence_after();
-    const uint32_t tmem_base = *tmem_holder;
-
-    if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer (both CTAs): own token half ----------------
-        const uint64_t keep = ptx::policy_evict_last();
-        int stage = 0;
-        uint32_t phase = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
-            const int t_row = (tile % num_t) * BN + static_cast<int>(rank) * (BN / 2);
-            for (int kb = 0; kb < num_kb; ++kb) {
-                ptx::mbar_wait(&empty[stage], phase ^ 1);
-                if (leader) ptx::mbar_arrive_expect_tx(&full[stage], 2 * L::b_half);
-                ptx::tma_load_2d_2sm(smem + stage * L::b_half, &tmX,
-                                     ptx::mapa(ptx::smem_u32(&full[stage]), 0), kb * BK, t_row, keep);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-            }
-        }
-    } else if (warp == 1 && lane == 0 && leader) {
-        // ---------------- MMA issuer (leader) ----------------
-        constexpr uint32_t idesc = ptx::idesc_i8(256, BN, /*b_unsigned=*/false, /*a_unsigned=*/true);
-        int stage = 0, as = 0, it = 0;
-        uint32_t phase = 0, aphase = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
-            const int acc = it % NACC;
-            FQG_TWAIT2(0, ptx::mbar_wait(&tempty[acc], ((it / NACC) & 1) ^ 1));
-            ptx::tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < num_kb; ++kb) {
-                FQG_TWAIT2(1, ptx::mbar_wait(&full[stage], phase));
-                FQG_TWAIT2(2, ptx::mbar_wait(&afull[as], aphase));
-                ptx::tc_fence_after();
-                const uint32_t a_tmem = tmem_base + L::a_col0 + as * 32;
-                const uint32_t b_addr = ptx::smem_u32(smem + stage * L::b_half);
-#pragma unroll
-                for (int k = 0; k < BK / UK; ++k)
-                    ptx::mma_i8_ts_pair(d_tmem, a_tmem + k * (UK / 4),
-                                        ptx::smem_desc_sw128_kmajor(b_addr + k * UK), idesc,
-                                        (kb | k) != 0 ? 1u : 0u);
-                ptx::mma_commit_pair(&empty[stage], 0x3);
-                ptx::mma_commit_pair(&aempty[as], 0x3);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
-                }
-                if (++as == AS) {
-                    as = 0;
-                    aphase ^= 1;
-                }
-            }
-            ptx::mma_commit_pair(&tfull[acc], 0x3);
-        }
-        if (dbg) atomicAdd(&g_dbg2[blockIdx.x % 296][3], clock64() - t_start);
-    } else if (warp >= 4 && warp < 8) {
-        // ---------------- epilogue (both CTAs): lane = feature, columns = tokens ----------------
-        const int q = warp - 4;
-        uint8_t* const ep0 = smem + L::epi_off + q * 2 * L::epi_buf;
-        const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);  // quantize.cpp:193
-        int it = 0, chunk = 0;
-        if (tma_y && lane == 0) ptx::tma_prefetch_desc(&tmY);
-        for (int tile = cid; tile < num_tiles; tile += ncl, ++it) {
-            const int f_blk = tile / num_t, t_blk = tile % num_t;
-            const int acc = it % NACC;
-            ptx::mbar_wait(&tfull[acc], (it / NACC) & 1);
-            ptx::tc_fence_after();
-            const int f0 = f_blk * 256 + static_cast<int>(rank) * 128 + 32 * q, feat = f0 + lane;
-            const bool fok = feat < n;
-            const double bv = (bias != nullptr && fok) ? load_bias(bias, bias_dt, feat) : 0.0;
-#pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c, ++chunk) {
-                uint32_t r[32];
-                if (!(dbg & 4))
-                    ptx::tmem_ld_32x32b_x32(
-                        tmem_base + (static_cast<uint32_t>(32 * q) << 16) + acc * BN + 32 * c, r);
-                const int t0 = t_blk * BN + 32 * c;
-                const int rs = t0 + lane < m ? rowsum[t0 + lane] : 0;
-                uint8_t* ep = ep0 + (chunk & 1) * L::epi_buf;
-                if (tma_y) {
-                    if (lane == 0) ptx::bulk_wait_read_allbut1();
-                    __syncwarp();
-                }
-                ptx::tmem_wait_ld();
-#pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const int corr = 8 * __shfl_sync(0xffffffffu, rs, j);
-                    *reinterpret_cast<OT*>(ep + j * L::epi_row + lane * ESZ) =
-                        convert_out<OUT>(static_cast<int32_t>(r[j]) - corr, s, bv);
-                }
-                if (tma_y) {
-                    ptx::fence_proxy_async_smem();
-                    __syncwarp();
-                    if (lane == 0) {
-                        ptx::tma_store_2d(&tmY, ep, f0, t0);
-                        ptx::bulk_commit();
-                    }
-                } else {
-                    __syncwarp();
-                    const int tok = t0 + lane;
-                    if (tok < m) {
-                        OT* dst = static_cast<OT*>(y) + static_cast<int64_t>(tok) * ldy + f0;
-                        for (int e = 0; e < 32 && f0 + e < n; ++e)
-                            dst[e] = *reinterpret_cast<const OT*>(ep + lane * L::epi_row + e * ESZ);
-                    }
-                    __syncwarp();
-                }
-            }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(ptx::mapa(ptx::smem_u32(&tempty[acc]), 0));
-        }
-        if (tma_y && lane == 0) ptx::bulk_wait_all();
-        if (dbg && lane == 0 && q == 0) atomicAdd(&g_dbg2[blockIdx.x % 296][4], clock64() - t_start);
-    } else if (warp >= 8) {
-        // ---------------- unpack teams (both CTAs): L2 -> registers -> own TMEM ----------------
-        const int team = (warp - 8) >> 2, q = warp & 3;
-        const int my_tiles = cid < num_tiles ? (num_tiles - 1 - cid) / ncl + 1 : 0;
-        const int steps = my_tiles * num_kb;
-        const uint32_t lead_afull = ptx::mapa(ptx::smem_u32(afull), 0);
-        auto load_step = [&](int st_i, uint4 (&v)[4]) {
-            if (st_i >= steps) return;
-            const int tile = cid + (st_i / num_kb) * ncl, kb = st_i % num_kb;
-            const int feat = (tile / num_t) * 256 + static_cast<int>(rank) * 128 + 32 * q + lane;
-            const uint8_t* wrow = w + static_cast<int64_t>(feat < n ? feat : 0) * ldb;
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int off = kb * (BK / 2) + 16 * i;
-                v[i] = (feat < n && off < kbytes) ? __ldg(reinterpret_cast<const uint4*>(wrow + off))
-                                                  : make_uint4(0u, 0u, 0u, 0u);
-            }
-        };
-        auto process = [&](int st_i, const uint4 (&v)[4]) {
-            const int as = st_i % AS;
-            uint32_t wd[32];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t pw[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    wd[8 * i + e] = pw[e] & 0x0F0F0F0Fu;             // k = 32i + 4e .. +3
-                    wd[8 * i + 4 + e] = (pw[e] >> 4) & 0x0F0F0F0Fu;  // k = 32i + 16 + 4e ..
-                }
-            }
-            if (dbg && lane == 0 && q == 0) {
-                FQG_TWAIT2(5 + team, ptx::mbar_wait(&aempty[as], ((st_i / AS) & 1) ^ 1));
-            }
-            __syncwarp();
-            ptx::mbar_wait(&aempty[as], ((st_i / AS) & 1) ^ 1);
-            ptx::tc_fence_after();
-            if (!(dbg & 2))
-                ptx::tmem_st_32x32b_x32(
-                    tmem_base + (static_cast<uint32_t>(32 * q) << 16) + L::a_col0 + as * 32, wd);
-            ptx::tmem_wait_st();
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive_cluster(lead_afull + as * 8);
-        };
-        uint4 va[4], vb[4], vc[4];
-        load_step(team, va);
-        load_step(team + 2, vb);
-        load_step(team + 4, vc);
-        for (int st_i = team; st_i < steps; st_i += 6) {
-            process(st_i, va);
-            load_step(st_i + 6, va);
-            if (st_i + 2 >= steps) break;
-            process(st_i + 2, vb);
-            load_step(st_i + 8, vb);
-            if (st_i + 4 >= steps) break;
-            process(st_i + 4, vc);
-            load_step(st_i + 10, vc);
-        }
-    }
-    ptx::tc_fence_before();
-    ptx::cluster_sync();
-    if (warp == 1) {
-        __syncwarp();
-        ptx::tc_fence_after();
-        ptx::tmem_dealloc_pair(tmem_base, 512);
-    }
-}
-
-// Split-K epilogue: y = epi(sum of the split planes), quantize.cpp:190-198
-// (+ the biased-int4 row-sum correction and the optional bias).
-template <int OUT>
-__global__ void __launch_bounds__(256)
-    k_splitk_reduce(const int32_t* __restrict__ ws, int splits, int m, int n, void* __restrict__ y,
-                    int64_t ldy, const double* __restrict__ scale, const void* __restrict__ bias,
-                    int bias_dt, const int32_t* __restrict__ rowsum) {
-    const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
-    const int64_t total = static_cast<int64_t>(m) * n;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        int32_t acc = 0;
-        for (int sp = 0; sp < splits; ++sp) acc += __ldcs(ws + sp * total + i);
-        const int row = static_cast<int>(i / n), col = static_cast<int>(i % n);
-        if (rowsum != nullptr) acc -= 8 * rowsum[row];
-        const double b = bias ? load_bias(bias, bias_dt, col) : 0.0;
-        store_one<OUT>(y, static_cast<int64_t>(row) * ldy + col, acc, s, b);
-    }
-}
-
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
-    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    static std::once_flag once;
-    std::call_once(once, [] {
-        void* p = nullptr;
-        cudaDriverEntryPointQueryResult q;
-        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
-                cudaSuccess &&
-            q == cudaDriverEntryPointSuccess)
-            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
-    });
-    if (!fn) throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled unavailable from the driver");
-    return fn;
-}
-
-template <int BN, int STAGES, int OUT, int AF, int BF>
-void launch(const GemmArgs& g, cudaStream_t stream) {
-    constexpr bool APK = AF != F8, BPK = BF != F8;
-    using L = Layout<BN, STAGES, APK, BPK>;
-    static_assert(L::total <= 227 * 1024, "shared memory budget");
-    CUtensorMap ta, tb;
-    // Logical K extent in bytes: the TMA zero-fills K' .. ceil(K', 128).
-    make_tmap_2d_u8(&ta, g.a, static_cast<uint64_t>(APK ? g.kp / 2 : g.kp),
-                    static_cast<uint64_t>(g.m), static_cast<uint64_t>(g.lda), APK ? BK / 2 : BK,
-                    BM, APK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(BPK ? g.kp / 2 : g.kp),
-                    static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.ldb), BPK ? BK / 2 : BK,
-                    BN, BPK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
-    auto kern = k_gemm_i8<BN, STAGES, OUT, AF, BF>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
-        attr_set = true;
-    }
-    int dev = 0;
-    FQG_CUDA(cudaGetDevice(&dev));
-    const int num_tiles = static_cast<int>(((g.m + BM - 1) / BM) * ((g.n + BN - 1) / BN));
-    const int grid = std::max(1, std::min(num_tiles, num_sms(dev)));
-    const int esz = dtype_size(g.y_dtype);
-    const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
-    const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
-    kern<<<grid, L::threads, L::total, stream>>>(ta, tb, g.y, g.ldy, static_cast<int>(g.m),
-                                                 static_cast<int>(g.n), num_kb, g.scale, g.bias,
-                                                 g.bias_dtype, vec ? 1 : 0, g.rowsum);
-    FQG_CUDA(cudaGetLastError());
-}
-
-template <int STAGES, int OUT, int AF, int BF, int NB>
-void launch_pair(const GemmArgs& g, cudaStream_t stream) {
-    constexpr bool APK = AF != F8, BPK = BF != F8;
-    using L = PairLayout<STAGES, APK, BPK, NB, epi_block_bytes<OUT>()>;
-    static_assert(L::total <= 227 * 1024, "shared memory budget");
-    CUtensorMap ta, tb;
-    make_tmap_2d_u8(&ta, g.a, static_cast<uint64_t>(APK ? g.kp / 2 : g.kp),
-                    static_cast<uint64_t>(g.m), static_cast<uint64_t>(g.lda), APK ? BK / 2 : BK,
-                    BM, APK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
-    make_tmap_2d_u8(&tb, g.b, static_cast<uint64_t>(BPK ? g.kp / 2 : g.kp),
-                    static_cast<uint64_t>(g.n), static_cast<uint64_t>(g.ldb), BPK ? BK / 2 : BK,
-                    L::BN / 2, BPK ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B);
-    auto kern = k_gemm_i8_pair<STAGES, OUT, AF, BF, NB>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
-        attr_set = true;
-    }
-    int dev = 0;
-    FQG_CUDA(cudaGetDevice(&dev));
-    const int num_tiles = static_cast<int>(((g.m + 2 * BM - 1) / (2 * BM)) *
-                                           ((g.n + NB * L::BN - 1) / (NB * L::BN)));
-    const int clusters = std::max(1, std::min(num_tiles, num_sms(dev) / 2));
-    const int esz = dtype_size(g.y_dtype);
-    const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
-    const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
-    static const int dbg = [] {
-        const char* e = std::getenv("FQG_GEMM_DEBUG");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (dbg) {
-        static unsigned long long zeros[296][8] = {};
-        FQG_CUDA(cudaMemcpyToSymbol(g_dbg, zeros, sizeof(zeros)));
-        FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
-    }
-    // Stream-K when whole tiles would leave a partial last round and every
-    // cluster's range still spans at least one full tile (two-way splits).
-    // Off by default: measured slower than data-parallel tiles on B200 (75 vs
-    // 61 us at 2048x4096x7488): the misaligned k offsets of the ranges cost more
-    // than the partial last round. FQG_GEMM_STREAMK=1 enables it.
-    static const int sk_env = [] {
-        const char* e = std::getenv("FQG_GEMM_STREAMK");
-        return e ? std::atoi(e) : 0;
-    }();
-    const int64_t units = static_cast<int64_t>(num_tiles) * num_kb;
-    int sk = (NB == 1 && sk_env != 0 && num_tiles > clusters && num_tiles % clusters != 0 &&
-              units / clusters >= num_kb)
-                 ? 1
-                 : 0;
-    // Split-K for small M: fewer than half the clusters would have a tile.
-    const int max_clusters = std::max(1, num_sms(dev) / 2);
-    if (sk == 0 && 2 * num_tiles <= max_clusters && num_kb >= 8) {
-        int splits = std::min({max_clusters / num_tiles, num_kb / 4, 8});
-        if (splits >= 2) sk = splits;
-    }
-    const int nclusters = sk >= 2 ? num_tiles * sk : clusters;
-    int32_t* ws = nullptr;
-    int* ws_flag = nullptr;
-    if (sk == 1) {
-        const int slots = nclusters + 1;
-        const size_t wbytes = static_cast<size_t>(slots) * 256 * (NB * L::BN) * 4;
-        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), wbytes + slots * 4, stream));
-        ws_flag = reinterpret_cast<int*>(reinterpret_cast<uint8_t*>(ws) + wbytes);
-        FQG_CUDA(cudaMemsetAsync(ws_flag, 0, slots * 4, stream));
-    } else if (sk >= 2) {
-        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws),
-                                 static_cast<size_t>(sk) * g.m * g.n * 4, stream));
-    }
-    CUtensorMap ty;
-    std::memset(&ty, 0, sizeof(ty));
-    const bool tma_y = epi_block_bytes<OUT>() > 0 && vec && sk < 2 && L::epi_groups == 1;
-    if (tma_y) {
-        const CUtensorMapDataType dt =
-            esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
-        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(g.m)};
-        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.ldy * esz)};
-        const cuuint32_t box[2] = {32, 32};
-        const cuuint32_t estr[2] = {1, 1};
-        const CUresult r = encode_fn()(&ty, dt, 2, g.y, dims, strides, box, estr,
-                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                       CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS)
-            throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed (" + std::to_string(r) + ")");
-    }
-    static const bool pdl = [] {
-        const char* e = std::getenv("FQG_PDL");
-        return !(e && std::atoi(e) == 0);
-    }();
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * nclusters);
-    cfg.blockDim = dim3(L::threads);
-    cfg.dynamicSmemBytes = L::total;
-    cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = pdl ? 1 : 0;
-    cudaError_t le = cudaLaunchKernelEx(
-        &cfg, kern, ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb,
-        g.scale, g.bias, g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk, ws, ws_flag, ty,
-        tma_y ? 1 : 0);
-    if (le == cudaSuccess) le = cudaGetLastError();
-    if (le == cudaSuccess && sk >= 2) {
-        const int64_t total = g.m * g.n;
-        const int rgrid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * num_sms(dev)));
-        k_splitk_reduce<OUT><<<rgrid, 256, 0, stream>>>(
-            ws, sk, static_cast<int>(g.m), static_cast<int>(g.n), g.y, g.ldy, g.scale, g.bias,
-            g.bias_dtype, BF == FU4 ? g.rowsum : nullptr);
-        le = cudaGetLastError();
-    }
-    if (ws) cudaFreeAsync(ws, stream);
-    FQG_CUDA(le);
-    if (dbg) {
-        unsigned long long h[296][8];
-        FQG_CUDA(cudaDeviceSynchronize());
-        FQG_CUDA(cudaMemcpyFromSymbol(h, g_dbg, sizeof(h)));
-        double acc[8] = {0};
-        const int nc = 2 * nclusters;
-        for (int c = 0; c < nc; ++c)
-            for (int i = 0; i < 8; ++i) acc[i] += static_cast<double>(h[c][i]) / nc;
-        // leader-only slots are averaged over both CTAs of a pair: x2
-        std::fprintf(stderr,
-                     "[fqg gemm pair] per leader: mma loop %.0f cyc for %.0f k-blocks (%.0f "
-                     "cyc/kb), start %.0f | mma wait-full %.0f wait-tempty %.0f | producer "
-                     "wait-empty %.0f | epi(thread) wait-tfull %.0f\n",
-                     acc[5] * 2, acc[6] * 2, acc[6] > 0 ? acc[5] / acc[6] : 0.0, acc[7] * 2,
-                     acc[1] * 2, acc[2] * 2, acc[0], acc[3] / 128);
-        std::fprintf(stderr, "[fqg gemm pair] SM clock during the MMA loop: %.0f MHz\n",
-                     acc[4] > 0 ? acc[5] / acc[4] * 1e3 : 0.0);
-        unsigned long long s0 = ~0ull, s1 = 0, e0 = ~0ull, e1 = 0;
-        for (int c = 0; c < nc; ++c) {
-            s0 = std::min<unsigned long long>(s0, h[c][0]);
-            s1 = std::max<unsigned long long>(s1, h[c][0]);
-            e0 = std::min<unsigned long long>(e0, h[c][3]);
-            e1 = std::max<unsigned long long>(e1, h[c][3]);
-        }
-        std::fprintf(stderr,
-                     "[fqg gemm pair] CTA start spread %.1f us, end spread %.1f..%.1f us after "
-                     "first start; per-leader mma loop %.1f us avg\n",
-                     (s1 - s0) * 1e-3, (e0 - s0) * 1e-3, (e1 - s0) * 1e-3, acc[4] * 2e-3);
-        for (int c = 0; c < nc; ++c)
-            if (h[c][3] - s0 > (e1 - s0) * 0.8 || (c >= 112 && c < 128))
-                std::fprintf(stderr,
-                             "[fqg gemm pair]   slow CTA %d (cluster %d, rank %d): start %.1f end %.1f us; "
-                             "mma loop %llu ns; epi %llu ns over %llu tiles\n",
-                             c, c / 2, c % 2, (h[c][0] - s0) * 1e-3, (h[c][3] - s0) * 1e-3, h[c][4],
-                             h[c][1], h[c][2]);
-        std::fprintf(stderr, "[fqg gemm pair] epilogue per tile (warp 0 of 4): %.2f us\n",
-                     acc[2] > 0 ? acc[1] / acc[2] * 1e-3 : 0.0);
-        unsigned long long h2[296][8];
-        FQG_CUDA(cudaMemcpyFromSymbol(h2, g_dbg2, sizeof(h2)));
-        double a2[8] = {0};
-        for (int c = 0; c < nc; ++c)
-            for (int i = 0; i < 8; ++i) a2[i] += static_cast<double>(h2[c][i]) / nc;
-        std::fprintf(stderr, "[fqg gemm pair] epilogue: accumulator ready at %.1f us, done at %.1f us (avg per CTA, summed over its tiles)\n",
-                     a2[6] * 1e-3, a2[7] * 1e-3);
-        std::fprintf(stderr,
-                     "[fqg gemm pair] per CTA: mma wait ufull %.0f, wait full_mma %.0f | unpack "
-                     "(thread 0): wait full_unp %.0f, wait uempty %.0f, work %.0f cyc over %.0f "
-                     "k-blocks\n",
-                     a2[0] * 2, a2[1] * 2, a2[2], a2[3], a2[4], a2[5]);
-    }
-}
-
-// Largest raw-ring depth (<= maxst) that fits the shared-memory budget.
-template <bool APK, bool BPK, int NB, int EPIB>
-constexpr int fit_stages(int maxst) {
-    using L1 = PairLayout<1, APK, BPK, NB, EPIB>;
-    const int fixed = L1::USTAGES * L1::unp_stage + 4 * 2 * EPIB + 1024 + 64 * 8 + 16;
-    const int st = (227 * 1024 - fixed) / L1::raw_stage;
-    return st < maxst ? st : maxst;
-}
-
-template <int AF, int BF, int NB, int OUT>
-void launch_pair_fit(const GemmArgs& g, cudaStream_t s) {
-    constexpr int ST = fit_stages<AF != F8, BF != F8, NB, epi_block_bytes<OUT>()>(6);
-    static_assert(ST >= 2, "pipeline depth");
-    launch_pair<ST, OUT, AF, BF, NB>(g, s);
-}
-
-template <int AF, int BF>
-void dispatch_pair(const GemmArgs& g, cudaStream_t s) {
-    // 256 x 512 tiles (NB = 2) when N is wide enough; FQG_GEMM_NB overrides.
-    static const int nb_env = [] {
-        const char* e = std::getenv("FQG_GEMM_NB");
-        return e ? std::atoi(e) : 0;
-    }();
-    // NB = 2 needs enough 256 x 512 tiles to fill the 74 CTA pairs; otherwise
-    // 256 x 256 tiles (plus split-K when even those are few).
-    const int64_t t2 = ((g.m + 255) / 256) * ((g.n + 511) / 512);
-    const int nb = nb_env ? nb_env : (g.n >= 512 && t2 >= 48 ? 2 : 1);
-    auto go = [&](auto nbc) {
-        constexpr int NB = decltype(nbc)::value;
-        switch (g.y_dtype) {
-            case FQG_I32: return launch_pair_fit<AF, BF, NB, FQG_I32>(g, s);
-            case FQG_F64: return launch_pair_fit<AF, BF, NB, FQG_F64>(g, s);
-            case FQG_F32: return launch_pair_fit<AF, BF, NB, FQG_F32>(g, s);
-            case FQG_F16: return launch_pair_fit<AF, BF, NB, FQG_F16>(g, s);
-            case FQG_BF16: return launch_pair_fit<AF, BF, NB, FQG_BF16>(g, s);
-            default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
-        }
-    };
-    if (nb == 2) return go(std::integral_constant<int, 2>{});
-    return go(std::integral_constant<int, 1>{});
-}
-
-template <int BN, int AF, int BF>
-void dispatch_out(const GemmArgs& g, cudaStream_t s) {
-    constexpr int ST = 4;
-    switch (g.y_dtype) {
-        case FQG_I32: return launch<BN, ST, FQG_I32, AF, BF>(g, s);
-        case FQG_F64: return launch<BN, ST, FQG_F64, AF, BF>(g, s);
-        case FQG_F32: return launch<BN, ST, FQG_F32, AF, BF>(g, s);
-        case FQG_F16: return launch<BN, ST, FQG_F16, AF, BF>(g, s);
-        case FQG_BF16: return launch<BN, ST, FQG_BF16, AF, BF>(g, s);
-        default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
-    }
-}
-
-template <int BN, int STAGES, int OUT>
-void launch_w4t(const GemmArgs& g, cudaStream_t stream) {
-    using L = W4Layout<BN, STAGES, sizeof(typename OutT<OUT>::T)>;
-    static_assert(L::total <= 227 * 1024, "shared memory budget");
-    CUtensorMap tx;
-    make_tmap_2d_u8(&tx, g.a, static_cast<uint64_t>(g.kp), static_cast<uint64_t>(g.m),
-                    static_cast<uint64_t>(g.lda), BK, BN, CU_TENSOR_MAP_SWIZZLE_128B);
-    auto kern = k_gemm_w4t<BN, STAGES, OUT>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
-        attr_set = true;
-    }
-    int dev = 0;
-    FQG_CUDA(cudaGetDevice(&dev));
-    const int num_tiles = static_cast<int>(((g.m + BN - 1) / BN) * ((g.n + 127) / 128));
-    const int grid = std::max(1, std::min(num_tiles, num_sms(dev)));
-    const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
-    const int esz = dtype_size(g.y_dtype);
-    const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
-    static const int dbg = [] {
-        const char* e = std::getenv("FQG_GEMM_DEBUG");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (dbg) {
-        static unsigned long long zeros[296][8] = {};
-        FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
-    }
-    // Output tiles leave by TMA tensor stores when y allows it (16-byte aligned
-    // base and row pitch).
-    CUtensorMap ty;
-    std::memset(&ty, 0, sizeof(ty));
-    const bool tma_y = vec;
-    if (tma_y) {
-        const CUtensorMapDataType dt = esz == 8   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
-                                       : esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
-                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
-        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(g.m)};
-        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.ldy * esz)};
-        const cuuint32_t box[2] = {32, 32};
-        const cuuint32_t estr[2] = {1, 1};
-        const CUresult r = encode_fn()(&ty, dt, 2, g.y, dims, strides, box, estr,
-                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                       CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS)
-            throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed (" + std::to_string(r) + ")");
-    }
-    kern<<<grid, L::threads, L::total, stream>>>(tx, static_cast<const uint8_t*>(g.b), g.ldb,
-                                                 static_cast<int>(g.kp / 2), g.y, g.ldy,
-                                                 static_cast<int>(g.m), static_cast<int>(g.n),
-                                                 num_kb, g.scale, g.bias, g.bias_dtype, g.rowsum,
-                                                 vec ? 1 : 0, dbg, ty, tma_y ? 1 : 0);
-    FQG_CUDA(cudaGetLastError());
-    if (dbg) {
-        unsigned long long h[296][8];
-        FQG_CUDA(cudaDeviceSynchronize());
-        FQG_CUDA(cudaMemcpyFromSymbol(h, g_dbg2, sizeof(h)));
-        double a[8] = {0};
-        for (int c = 0; c < grid; ++c)
-            for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[c][i]) / grid;
-        std::fprintf(stderr,
-                     "[fqg gemm w4t] per CTA cycles: mma wait tempty %.0f, wait full(x) %.0f, wait "
-                     "afull(w) %.0f | epilogue wait tfull %.0f, work %.0f | unpack wait aempty "
-                     "team0 %.0f team1 %.0f | %d k-blocks/tile\n",
-                     a[0], a[1], a[2], a[3], a[4], a[5], a[6], num_kb);
-    }
-}
-
-void dispatch_w4t(const GemmArgs& g, cudaStream_t s) {
-    constexpr int BN = 192, ST = 6;
-    switch (g.y_dtype) {
-        case FQG_I32: return launch_w4t<BN, ST, FQG_I32>(g, s);
-        case FQG_F64: return launch_w4t<BN, ST, FQG_F64>(g, s);
-        case FQG_F32: return launch_w4t<BN, ST, FQG_F32>(g, s);
-        case FQG_F16: return launch_w4t<BN, ST, FQG_F16>(g, s);
-        case FQG_BF16: return launch_w4t<BN, ST, FQG_BF16>(g, s);
-        default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
-    }
-}
-
-template <int BN, int STAGES, int OUT, int NACC>
-void launch_w4t_pair(const GemmArgs& g, cudaStream_t stream) {
-    using L = W4PairLayout<BN, STAGES, sizeof(typename OutT<OUT>::T), NACC>;
-    static_assert(L::total <= 227 * 1024, "shared memory budget");
-    CUtensorMap tx;
-    make_tmap_2d_u8(&tx, g.a, static_cast<uint64_t>(g.kp), static_cast<uint64_t>(g.m),
-                    static_cast<uint64_t>(g.lda), BK, BN / 2, CU_TENSOR_MAP_SWIZZLE_128B);
-    auto kern = k_gemm_w4t_pair<BN, STAGES, OUT, NACC>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L::total));
-        attr_set = true;
-    }
-    int dev = 0;
-    FQG_CUDA(cudaGetDevice(&dev));
-    const int num_tiles = static_cast<int>(((g.m + BN - 1) / BN) * ((g.n + 255) / 256));
-    const int clusters = std::max(1, std::min(num_tiles, num_sms(dev) / 2));
-    const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
-    const int esz = dtype_size(g.y_dtype);
-    const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
-    CUtensorMap ty;
-    std::memset(&ty, 0, sizeof(ty));
-    if (vec) {
-        const CUtensorMapDataType dt = esz == 8   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
-                                       : esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
-                                                  : CU_TENSOR_MAP_DATA_TYPE_UINT16;
-        const cuuint64_t dims[2] = {static_cast<cuuint64_t>(g.n), static_cast<cuuint64_t>(g.m)};
-        const cuuint64_t strides[1] = {static_cast<cuuint64_t>(g.ldy * esz)};
-        const cuuint32_t box[2] = {32, 32};
-        const cuuint32_t estr[2] = {1, 1};
-        const CUresult r = encode_fn()(&ty, dt, 2, g.y, dims, strides, box, estr,
-                                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                       CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-        if (r != CUDA_SUCCESS)
-            throw Error(FQG_ERR_CUDA, "cuTensorMapEncodeTiled (y) failed (" + std::to_string(r) + ")");
-    }
-    static const int dbg = [] {
-        const char* e = std::getenv("FQG_GEMM_DEBUG");
-        return e ? std::atoi(e) : 0;
-    }();
-    if (dbg) {
-        static unsigned long long zeros[296][8] = {};
-        FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
-    }
-    kern<<<2 * clusters, L::threads, L::total, stream>>>(
-        tx, static_cast<const uint8_t*>(g.b), g.ldb, static_cast<int>(g.kp / 2), g.y, g.ldy,
-        static_cast<int>(g.m), static_cast<int>(g.n), num_kb, g.scale, g.bias, g.bias_dtype,
-        g.rowsum, ty, vec ? 1 : 0, dbg);
-    FQG_CUDA(cudaGetLastError());
-    if (dbg) {
-        unsigned long long h[296][8];
-        FQG_CUDA(cudaDeviceSynchronize());
-        FQG_CUDA(cudaMemcpyFromSymbol(h, g_dbg2, sizeof(h)));
-        double a[8] = {0};
-        for (int c = 0; c < 2 * clusters; ++c)
-            for (int i = 0; i < 8; ++i) a[i] += static_cast<double>(h[c][i]) / (2 * clusters);
-        std::fprintf(stderr,
-                     "[fqg gemm w4t_pair] per CTA cycles (leader-only x2): mma wait tempty %.0f, "
-                     "full(x) %.0f, afull(w) %.0f, mma loop end %.0f | epilogue end %.0f | unpack "
-                     "wait aempty %.0f / %.0f | tiles %d, k-blocks %d\n",
-                     2 * a[0], 2 * a[1], 2 * a[2], 2 * a[3], a[4], a[5], a[6], num_tiles, num_kb);
-    }
-}
-
-// Pair tile 256 features x 256 tokens, one accumulator (MMA 256x256x32 in TS
-// mode: 4563 TOPS measured vs 2900 at N = 160, tools/mma_ts.cu).
-void dispatch_w4t_pair(const GemmArgs& g, cudaStream_t s) {
-    constexpr int BN = 256, ST = 8, NA = 1;
-    switch (g.y_dtype) {
-        case FQG_I32: return launch_w4t_pair<BN, ST, FQG_I32, NA>(g, s);
-        case FQG_F64: return launch_w4t_pair<BN, ST, FQG_F64, NA>(g, s);
-        case FQG_F32: return launch_w4t_pair<BN, ST, FQG_F32, NA>(g, s);
-        case FQG_F16: return launch_w4t_pair<BN, ST, FQG_F16, NA>(g, s);
-        case FQG_BF16: return launch_w4t_pair<BN, ST, FQG_BF16, NA>(g, s);
-        default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
-    }
-}
-
-int kfmt(int f) { return f == FQG_I8 ? F8 : (f == FQG_I4 ? FS4 : FU4); }
-
-void dispatch_pair_fmt(const GemmArgs& g, cudaStream_t s) {
+void dispatch_pair_fmt(const GemmArgs& g, const GemmPlan& p, cudaStream_t s) {
     const int af = kfmt(g.a_fmt), bf = kfmt(g.b_fmt);
-    if (af == F8 && bf == F8) return dispatch_pair<F8, F8>(g, s);
-    if (af == F8 && bf == FS4) return dispatch_pair<F8, FS4>(g, s);
-    if (af == F8 && bf == FU4) return dispatch_pair<F8, FU4>(g, s);
-    if (af == FS4 && bf == F8) return dispatch_pair<FS4, F8>(g, s);
-    if (af == FS4 && bf == FS4) return dispatch_pair<FS4, FS4>(g, s);
-    return dispatch_pair<FS4, FU4>(g, s);
+    if (af == F8 && bf == F8) return gemm_pair_F8_F8(g, p, s);
+    if (af == F8 && bf == FS4) return gemm_pair_F8_FS4(g, p, s);
+    if (af == F8 && bf == FU4) return gemm_pair_F8_FU4(g, p, s);
+    if (af == FS4 && bf == F8) return gemm_pair_FS4_F8(g, p, s);
+    if (af == FS4 && bf == FS4) return gemm_pair_FS4_FS4(g, p, s);
+    return gemm_pair_FS4_FU4(g, p, s);
 }
-
-template <int BN>
-void dispatch_fmt(const GemmArgs& g, cudaStream_t s) {
-    const int af = kfmt(g.a_fmt), bf = kfmt(g.b_fmt);
-    if (af == F8 && bf == F8) return dispatch_out<BN, F8, F8>(g, s);
-    if (af == F8 && bf == FS4) return dispatch_out<BN, F8, FS4>(g, s);
-    if (af == F8 && bf == FU4) return dispatch_out<BN, F8, FU4>(g, s);
-    if (af == FS4 && bf == F8) return dispatch_out<BN, FS4, F8>(g, s);
-    if (af == FS4 && bf == FS4) return dispatch_out<BN, FS4, FS4>(g, s);
-    return dispatch_out<BN, FS4, FU4>(g, s);
-}
-
 }  // namespace
+
 
 void make_tmap_2d_u8(CUtensorMap* map, const void* base, uint64_t inner_bytes, uint64_t rows,
                      uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_rows,
@@ -1970,30 +54,61 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
     require(g.kp % 32 == 0, "gemm: K' must be a multiple of 32");
     // INT32 exactness: |acc| <= K' * 127 * 127 must stay below 2^31.
     require(g.kp * 127ll * 127ll < (1ll << 31), "gemm: K' too large for exact INT32 accumulation");
-    // variant: 0 auto, 1 single-CTA 128 x BN tiles, 2 CTA-pair 256 x 256 tiles.
-    // FQG_GEMM_VARIANT overrides auto (tests exercise both kernels).
+    int dev = 0;
+    FQG_CUDA(cudaGetDevice(&dev));
+    const GemmPlan p = plan_gemm(g.m, g.n, g.kp, g.a_fmt, g.b_fmt, g.variant, num_sms(dev));
+    if (p.kernel == 2)
+        dispatch_pair_fmt(g, p, stream);
+    else if (kfmt(g.a_fmt) == F8)
+        gemm_one_F8(g, p.tile_n, stream);
+    else
+        gemm_one_FS4(g, p.tile_n, stream);
+}
+
+GemmPlan plan_gemm(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int variant, int sms) {
+    // variant: 0 auto, 1 single-CTA 128 x BN tiles, 2 CTA-pair kernel.
+    // FQG_GEMM_VARIANT / FQG_GEMM_NB override auto (tuning experiments).
     static const int env_variant = [] {
         const char* e = std::getenv("FQG_GEMM_VARIANT");
         return e ? std::atoi(e) : 0;
     }();
-    int v = g.variant != 0 ? g.variant : env_variant;
+    static const int nb_env = [] {
+        const char* e = std::getenv("FQG_GEMM_NB");
+        return e ? std::atoi(e) : 0;
+    }();
+    GemmPlan p{};
+    int v = variant != 0 ? variant : env_variant;
     // Measured at 2048 x 4096 x 7488: pair 61 us (int8 weights) / 71 us (biased
-    // int4), single-CTA 71 us (int4), weights-in-TMEM 87 us (int4).
-    if (v == 0)
-        v = (g.m > BM && g.n > 128 && g.a_fmt == FQG_I8 &&
-             (g.b_fmt == FQG_I8 || g.b_fmt == FQG_I4_BIASED))
-                ? 2
-                : 1;
-    if (v == 3 && g.a_fmt == FQG_I8 && g.b_fmt == FQG_I4_BIASED)
-        dispatch_w4t(g, stream);
-    else if (v == 4 && g.a_fmt == FQG_I8 && g.b_fmt == FQG_I4_BIASED)
-        dispatch_w4t_pair(g, stream);
-    else if (v == 2)
-        dispatch_pair_fmt(g, stream);
-    else if (g.n <= 128)
-        dispatch_fmt<128>(g, stream);
-    else
-        dispatch_fmt<256>(g, stream);
+    // int4), single-CTA 71 us (int4); a weights-in-TMEM variant (unpacked int4
+    // weights as the MMA's A operand in TMEM) measured 79-87 us and was removed.
+    if (v == 0) v = (m > BM && n > 128 && a_fmt == FQG_I8) ? 2 : 1;
+    const int64_t num_kb = (kp + BK - 1) / BK;
+    if (v == 2) {
+        p.kernel = 2;
+        p.tile_m = 2 * BM;
+        // 256 x 512 tiles (NB = 2) need enough tiles to fill the CTA pairs;
+        // otherwise 256 x 256 (plus split-K when even those are few).
+        const int64_t t2 = ((m + 255) / 256) * ((n + 511) / 512);
+        const int nb = nb_env ? nb_env : (n >= 512 && t2 >= 48 ? 2 : 1);
+        p.tile_n = 256 * nb;
+        const int64_t tiles = ((m + 255) / 256) * ((n + p.tile_n - 1) / p.tile_n);
+        const int64_t pairs = std::max(1, sms / 2);
+        // Split-K for small M: fewer than half the pairs would have a tile.
+        if (nb == 1 && 2 * tiles <= pairs && num_kb >= 8) {
+            const int64_t sp = std::min<int64_t>({pairs / tiles, num_kb / 4, 8});
+            if (sp >= 2) p.splits = static_cast<int>(sp);
+        }
+        p.ctas = static_cast<int>(2 * (p.splits >= 2 ? tiles * p.splits
+                                                     : std::max<int64_t>(1, std::min(tiles, pairs))));
+    } else {
+        p.kernel = 1;
+        p.tile_m = BM;
+        p.tile_n = n <= 128 ? 128 : 256;
+        const int64_t tiles = ((m + BM - 1) / BM) * ((n + p.tile_n - 1) / p.tile_n);
+        p.ctas = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(tiles, sms)));
+    }
+    return p;
 }
 
 }  // namespace fqg
+

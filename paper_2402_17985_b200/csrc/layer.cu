@@ -126,6 +126,12 @@ fqg_layer_s* create(const fqg_layer_desc& d) {
         L->qmax = static_cast<double>((1 << (d.bits - 1)) - 1);
         const Plan px = plan_from_ext(d.t_x, d.ext_x, d.k, d.block_x);
         const Plan pw = plan_from_ext(d.t_w, d.ext_w, px.padded, d.block_w);
+        // The GEMM consumes K' in steps of 32 (tcgen05 kind::i8 K) and packs int4
+        // in groups of 32; both padded widths must be 32-aligned (the reference's
+        // default block, flatten.hpp:20). Checked before any packing or upload.
+        if (px.padded % 32 != 0 || pw.padded % 32 != 0)
+            throw Error(FQG_ERR_UNSUPPORTED,
+                        "layer: plan padded widths must be multiples of 32 (block_x/block_w)");
         L->c1 = px.padded;
         L->kp = pw.padded;
         const GatherMaps g = compile_maps(px, pw);
@@ -335,6 +341,7 @@ void run_gemm(const fqg_layer_s* L, const void* q, const int32_t* rowsum, int64_
     GemmArgs g{q, L->a_fmt, ldq_of(L), L->d_wq.p, biased_b(L) ? FQG_I4_BIASED : L->b_fmt, L->ldb,
                m, L->n, L->kp, y, y_dtype, ldy, scale, bias, bias ? bias_dtype : FQG_NONE};
     g.rowsum = rowsum;
+    g.qmax_a = g.qmax_b = static_cast<int>(L->qmax);  // both operands hold bits-wide values
     try {
         gemm_i8(g, st);
     } catch (...) {
@@ -512,8 +519,12 @@ int fqg_layer_run_host(fqg_layer_t L, const double* x_host, int64_t m, double* y
         FQG_CUDA(cudaMemsetAsync(dsat, 0, 8, st));
         FQG_CUDA(cudaEventRecord(ev[0], st));  // allocations + zeroed counter visible to stream 1
         FQG_CUDA(cudaStreamWaitEvent(ss[1], ev[0], 0));
-        // ~8 chunks of >= 128 rows (a multiple of 32 keeps the GEMM tiles full)
-        const int64_t chunk = std::max<int64_t>(128, ((m + 7) / 8 + 31) / 32 * 32);
+        // ~8 chunks of >= 128 rows (a multiple of 32 keeps the GEMM tiles full).
+        // The dynamic scale is one absmax over the whole input (quantize.cpp:34-40):
+        // a single chunk then, so every row sees the same s_x.
+        const int64_t chunk = L->scale_mode == FQG_SCALE_DYNAMIC
+                                  ? m
+                                  : std::max<int64_t>(128, ((m + 7) / 8 + 31) / 32 * 32);
         int ci = 0;
         for (int64_t r0 = 0; r0 < m; r0 += chunk, ++ci) {
             const int64_t mc = std::min(chunk, m - r0);

@@ -267,9 +267,10 @@ def _rn_bf16(v):
 
 
 @pytest.mark.parametrize("sx,sw", [(2.0 ** -10, 1.0), (2.0 ** -14, 0.5), (3.7e-5, 0.0123),
-                                   (1.0 / 3.0, 0.9), (2.0 ** -30, 1.0)])
+                                   (1.0 / 3.0, 0.9), (2.0 ** -30, 1.0), (2.0 ** -3, 1.0)])
 @pytest.mark.parametrize("out", ["f16", "bf16"])
-def test_half_outputs_are_rn16_of_reference(fq, sx, sw, out):
+@pytest.mark.parametrize("b_fmt", ["i8", "i4"])
+def test_half_outputs_are_rn16_of_reference(fq, sx, sw, out, b_fmt):
     """2-byte outputs equal RN16(double(acc) * (s_x * s_w)) exactly (quantize.cpp:193-196
     rounded once). The epilogue's certified fp32 fast path must defer every element
     near a rounding midpoint: power-of-two scales make ~half of them exact ties;
@@ -281,13 +282,20 @@ def test_half_outputs_are_rn16_of_reference(fq, sx, sw, out):
     m, n, kp = 512, 1024, 1536
     g = torch.Generator().manual_seed(int(sx * 1e6) + n)
     a = torch.randint(-127, 128, (m, kp), dtype=torch.int8, generator=g)
-    b = torch.randint(-127, 128, (n, kp), dtype=torch.int8, generator=g)
+    if b_fmt == "i8":  # |acc| up to 2^24.6: the split int -> float path of the epilogue
+        b = torch.randint(-127, 128, (n, kp), dtype=torch.int8, generator=g)
+        bdev, bcode, ldb = b.cuda(), _lib.I8, kp
+    else:  # packed int4 weights, |acc| < 2^22: the one-FADD int -> float path
+        b = torch.randint(-7, 8, (n, kp), dtype=torch.int8, generator=g)
+        nib = (b.numpy().astype(np.int32) & 15).reshape(n, kp // 32, 2, 16)
+        packed = (nib[:, :, 0, :] | (nib[:, :, 1, :] << 4)).astype(np.uint8).reshape(n, kp // 2)
+        bdev, bcode, ldb = torch.from_numpy(packed.view(np.int8)).cuda(), _lib.I4, kp // 2
     acc = a.numpy().astype(np.int64) @ b.numpy().astype(np.int64).T
     v = acc.astype(np.float64) * (sx * sw)
     scale = torch.tensor([sx, sw], dtype=torch.float64, device="cuda")
     tdt = torch.float16 if out == "f16" else torch.bfloat16
     y = torch.empty((m, n), dtype=tdt, device="cuda")
-    fq.check(fq.lib().fqg_gemm(a.cuda().data_ptr(), _lib.I8, kp, b.cuda().data_ptr(), _lib.I8, kp,
+    fq.check(fq.lib().fqg_gemm(a.cuda().data_ptr(), _lib.I8, kp, bdev.data_ptr(), bcode, ldb,
                                m, n, kp, y.data_ptr(), _lib.F16 if out == "f16" else _lib.BF16, n,
                                scale.data_ptr(), None, _lib.NONE,
                                torch.cuda.current_stream().cuda_stream))

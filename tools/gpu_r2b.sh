@@ -1,0 +1,8 @@
+set -x
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_epilogue.py -x -q 2>&1 | tail -5
+timeout 900 python -m pytest tests/test_gpu_full.py -x -q 2>&1 | tail -5
+for d in 1 17; do FQG_GEMM_DEBUG=$d timeout 120 python tools/layer_gemm_dbg.py 2>&1 | tail -9; done
+FQG_GEMM_DEBUG=1 timeout 120 python tools/layer_gemm_dbg.py 5 2>&1 | tail -9
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench.json; cat gpurun_out/bench.json
+timeout 900 python -m pytest tests -x -q -m gpu 2>&1 | tail -3

@@ -1,0 +1,6 @@
+set -x
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_epilogue.py tests/test_gpu_parity.py -x -q -k "epilogue or rn16 or bias" 2>&1 | tail -5
+timeout 900 python -m pytest tests/test_gpu_full.py -x -q 2>&1 | tail -5
+for d in 1 17; do FQG_GEMM_DEBUG=$d timeout 120 python tools/layer_gemm_dbg.py 2>&1 | tail -3; done
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --e2e-steps 2 > gpurun_out/bench.json; python -c "import json;d=json.load(open('gpurun_out/bench.json'));print(d['value'],d['breakdown_ms'],d['roofline']['frac'])"
