@@ -39,6 +39,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -144,80 +145,51 @@ __device__ __forceinline__ uint32_t pack_i4_word(uint32_t lo, uint32_t hi) {
     return (lo & 0x0F0F0F0Fu) | ((hi << 4) & 0xF0F0F0F0u);
 }
 
-// K1 layout: a CTA of kWarps warps forms row teams of TW threads (TW / 32
-// warps, synchronised by a named barrier); each team streams its own token
-// rows. The CTA shares the per-channel certificate in shared memory; each team
-// owns its final operand row (+ a zero byte at column K' for padding copies),
-// its int4 packing, a tier-2 queue and a long-run list. x streams straight
-// into registers (16-byte loads, the next chunk in flight while the current
-// one is computed); finished rows leave by bulk stores. Splitting a row over
-// several warps shortens the per-row dependency chain, which (with all rows
-// in flight at once) is what bounds this kernel.
-constexpr int kWarps = 8;     // warps per CTA
-constexpr int kCh = 8;        // 16-byte x loads per thread per chunk (= 8 channel groups)
-constexpr int kInline = 6;    // extension runs up to this long are written by their thread
-constexpr int kRunCap = 32;   // longer runs are listed and written by the whole team
-constexpr int kQCap = 128;    // tier-2 queue entries per team
+// K1 layout: a CTA of 256 threads owns a block of R token rows (R in {1, 2,
+// 4, 8}, chosen from M so that every SM holds several blocks at once). Every
+// phase spreads the block's elements over all threads, so no thread carries a
+// row's whole dependency chain:
+//   1. tier 1   thread t takes channel groups g = t, t + 256, ... (8 channels,
+//               one 16-byte x load per row, the R rows' loads in flight
+//               together); certificate c_j / P_j loaded once per group and
+//               reused for the R rows; slot bytes go to the row buffers in SMEM.
+//               Tier-2 elements only set a bit in the row's SMEM bitmap.
+//   2. splits   the "hot" channels (calibrated maximum >= 4 T_x: exact path on
+//               every row, from a per-layer list) and the bitmap's elements run
+//               the exact split of split.cuh: piece 0 into slot j and the run of
+//               extension pieces (count full +-q(T) pieces, then q(rem);
+//               flatten.cpp:71-72) into the channel's slots K + off_j ...
+//               (the slots [K, C1) are zeroed at block start).
+//   3. copies   plan_w copies [C1, K') (repeat_columns, flatten.cpp:158-174):
+//               byte gathers from the finished row.
+//   4. store    int4 packing in place (packed activations), then one bulk copy
+//               per row to HBM.
+// The per-row operand sums (biased-int4 GEMM epilogue) are accumulated on the
+// way (dp4a of the tier-1 words and copy words, corrections and extension
+// pieces of the splits) instead of by a re-read of the rows.
+constexpr int kThreads = 256;
 constexpr int kMaxHot = 128;  // hot channels (layer.cu caps the list)
-
-struct K1Smem {
-    uint32_t cj, pj, wsrc, hotm, hotg, tbar, per_team0, fl, pk, queue, runs, hotx, per_team, total;
-    uint32_t hotg_bytes;
-    int ldf;
-};
-K1Smem k1_smem(int k, int kp, int c1, bool pack4, int teams) {
-    K1Smem w{};
-    uint32_t o = 0;
-    auto take = [&](uint32_t& at, uint32_t bytes) {
-        at = o;
-        o = (o + bytes + 15) & ~15u;
-    };
-    take(w.cj, static_cast<uint32_t>(k) * 4);
-    take(w.pj, static_cast<uint32_t>(k) * 2);
-    take(w.wsrc, static_cast<uint32_t>(kp - c1) * 4);
-    take(w.hotm, kMaxHot * 16);
-    w.hotg_bytes = static_cast<uint32_t>((k / 8 + 3) / 4 * 16);
-    take(w.hotg, w.hotg_bytes);
-    take(w.tbar, 16);
-    w.per_team0 = o;
-    w.ldf = kp + 16;
-    o = 0;
-    take(w.fl, static_cast<uint32_t>(w.ldf));
-    take(w.pk, pack4 ? static_cast<uint32_t>(kp) / 2 : 0u);
-    take(w.queue, kQCap * 8);
-    take(w.runs, kRunCap * 16);
-    take(w.hotx, kMaxHot * 2);
-    w.per_team = o;
-    w.total = w.per_team0 + teams * w.per_team;
-    return w;
-}
+constexpr int kListCap = 1024;  // compacted tier-2 elements per block
 
 struct K16Params {
     const void* x;
     int64_t ldx;
     int m, k, kp, c1, ldf, nhot;
-    uint32_t s_cj, s_pj, s_wsrc, s_hotm, s_hotg, s_tbar, hotg_bytes, per_team0, fl, pk, queue, runs,
-        hotx, per_team;
     const float* cj;
     const uint16_t* pj;
-    const int32_t* hot;   // channels taking the exact path on every row (P_j = 0xFFFF)
-    const int32_t* hotm;  // [nhot] {j, cap, off, rs32 bits}
-    const int32_t* hotg;  // [k / 8] group hot mask | first hot index << 8
-    const int32_t* off;   // [k] plan_x ext_offset
-    const int32_t* wsrc;  // [kp - c1] flat column of each plan_w copy (padding -> kp, a zero byte)
+    const int32_t* hotm;   // [nhot] {j, cap, off, rs32 bits}
+    const int32_t* off;    // [k] plan_x ext_offset
+    const int32_t* wsrc;   // [kp - c1] flat column of each plan_w copy (padding -> kp, a zero byte)
     const double* s;
     const double* rs;
-    const float* rs32;
     const int32_t* cap;
-    SplitConsts sc;       // host-computed (identical IEEE arithmetic)
+    const float* rs32;
+    SplitConsts sc;        // host-computed (identical IEEE arithmetic)
     uint8_t* q;
     int64_t ldq;
     unsigned long long* sat;
     int32_t* rowsum;
-    int dbg;
 };
-
-__device__ unsigned long long g_k1dbg[16];
 
 // Extension pieces 1 .. last of one element into d[0 .. last): full pieces
 // (value fv) for p < ce, the remainder qe at p == ce (flatten.cpp:71-72);
@@ -231,122 +203,65 @@ __device__ __forceinline__ void fill_pieces(int8_t* d, int last, int ce, int fv,
     for (; p + 4 <= nfull; p += 4) *reinterpret_cast<uint32_t*>(d + p) = word;
     for (; p < nfull; ++p) d[p] = static_cast<int8_t>(fv);
     if (ce <= last) d[ce - 1] = static_cast<int8_t>(qe);
-}  // FQG_K1_DEBUG: summed phase end times (cycles)
-
-template <int TW>
-__device__ __forceinline__ void team_sync(int team) {
-    if constexpr (TW == 32)
-        __syncwarp();
-    else
-        asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "n"(TW) : "memory");
 }
 
-template <bool F16, bool PACK4, int TW>
-__global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_constant__ K16Params p) {
-    constexpr int TEAMS = kWarps * 32 / TW;
-    const long long t_start = clock64();
+template <bool F16, bool PACK4, int R>
+__global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __grid_constant__ K16Params p) {
     ptx::griddep_launch_dependents();  // K4 may start its prologue (it waits for our stores)
-    auto mark = [&](int slot) {
-        if (p.dbg && (threadIdx.x % TW) == 0) atomicAdd(&g_k1dbg[slot], clock64() - t_start);
-    };
     extern __shared__ __align__(16) uint8_t sm[];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int team = tid / TW, tt = tid % TW;
-    const float* const scj = reinterpret_cast<const float*>(sm + p.s_cj);
-    const uint16_t* const spj = reinterpret_cast<const uint16_t*>(sm + p.s_pj);
-    const int4* const swsrc = reinterpret_cast<const int4*>(sm + p.s_wsrc);
-    const int4* const shot = reinterpret_cast<const int4*>(sm + p.s_hotm);  // {j, cap, off, rs32}
-    const int32_t* const shotg = reinterpret_cast<const int32_t*>(sm + p.s_hotg);
-    uint8_t* const base = sm + p.per_team0 + team * p.per_team;
-    int8_t* const fl = reinterpret_cast<int8_t*>(base + p.fl);
-    uint8_t* const pk = base + p.pk;
-    uint2* const queue = reinterpret_cast<uint2*>(base + p.queue);
-    uint4* const runs = reinterpret_cast<uint4*>(base + p.runs);
-    uint16_t* const hotx = reinterpret_cast<uint16_t*>(base + p.hotx);
-    __shared__ int qlen_s[TEAMS], nrun_s[TEAMS], rsum_s[TEAMS];
-    int& qlen = qlen_s[team];
-    int& nrun = nrun_s[team];
-    int& rsum_t = rsum_s[team];
-
-    const int k = p.k, kp = p.kp, c1 = p.c1, ng_all = k >> 3;
+    const int tid = threadIdx.x;
+    const int k = p.k, kp = p.kp, c1 = p.c1, ldf = p.ldf;
+    const int ngrp = k >> 3, nbw = (ngrp + 3) >> 2;  // channel groups, bitmap words per row
+    const int row0 = blockIdx.x * R;
+    const int nrow = min(R, p.m - row0);
     const SplitConsts& sc = p.sc;
-    const int full = sc.qT;
-    const int worker = blockIdx.x * TEAMS + team, nworkers = gridDim.x * TEAMS;
-    const int nch = (ng_all + TW * kCh - 1) / (TW * kCh);  // chunks per row
-    const int nrows_w = worker < p.m ? (p.m - 1 - worker) / nworkers + 1 : 0;
-    const int nchunks = nrows_w * nch;
-    const uint4* x4 = static_cast<const uint4*>(p.x);
-    const int64_t ldx4 = p.ldx >> 3;
-
-    auto load_chunk = [&](uint4 (&buf)[kCh], int t) {
-        if (t >= nchunks) return;
-        const int row = worker + (t / nch) * nworkers, c = t % nch;
-        const uint4* src = x4 + static_cast<int64_t>(row) * ldx4;
+    int8_t* const rows = reinterpret_cast<int8_t*>(sm);                     // [R][ldf]
+    uint32_t* const bitmap = reinterpret_cast<uint32_t*>(sm + R * ldf);      // [R][nbw]
+    uint8_t* const bitmap8 = reinterpret_cast<uint8_t*>(bitmap);
+    __shared__ uint32_t list[kListCap];  // compacted tier-2 elements: r << 24 | j
+    __shared__ int rsum_s[R];
+    __shared__ int qlen;
+    if (tid < R) rsum_s[tid] = 0;
+    if (tid == 0) qlen = 0;
+    {  // zero the plan_x extension slots [K, C1), the tier-2 bitmap, and the byte
+       // at K' (plan_w padding copies read it)
+        const int z0 = (k + 15) & ~15;
 #pragma unroll
-        for (int i = 0; i < kCh; ++i) {
-            const int g = (c * kCh + i) * TW + tt;
-            if (g < ng_all) buf[i] = __ldg(src + g);
+        for (int r = 0; r < R; ++r)
+            for (int u = tid; u < ((c1 - z0) >> 4); u += kThreads)
+                *reinterpret_cast<uint4*>(rows + r * ldf + z0 + 16 * u) = make_uint4(0u, 0u, 0u, 0u);
+        for (int u = tid; u < R * nbw; u += kThreads) bitmap[u] = 0u;
+        if (tid < R) {
+            if (z0 != k) *reinterpret_cast<uint2*>(rows + tid * ldf + k) = make_uint2(0u, 0u);
+            rows[tid * ldf + kp] = 0;
         }
-    };
-
-    // the first x chunk is in flight while the tables are staged
-    uint4 xa[kCh], xb[kCh];
-    load_chunk(xa, 0);
-
-    // stage the per-layer tables (shared by the CTA's teams) with 1-D bulk copies
-    uint64_t* tbar = reinterpret_cast<uint64_t*>(sm + p.s_tbar);
-    if (tid == 0) {
-        ptx::mbar_init(tbar, 1);
-        ptx::fence_barrier_init();
-        const uint32_t b_cj = static_cast<uint32_t>(k) * 4, b_pj = static_cast<uint32_t>(k) * 2;
-        const uint32_t b_ws = static_cast<uint32_t>(kp - c1) * 4;
-        const uint32_t b_hm = static_cast<uint32_t>(p.nhot) * 16;
-        ptx::mbar_arrive_expect_tx(tbar, b_cj + b_pj + b_ws + b_hm + p.hotg_bytes);
-        ptx::bulk_load(sm + p.s_cj, p.cj, b_cj, tbar);
-        ptx::bulk_load(sm + p.s_pj, p.pj, b_pj, tbar);
-        if (b_ws) ptx::bulk_load(sm + p.s_wsrc, p.wsrc, b_ws, tbar);
-        if (b_hm) ptx::bulk_load(sm + p.s_hotm, p.hotm, b_hm, tbar);
-        ptx::bulk_load(sm + p.s_hotg, p.hotg, p.hotg_bytes, tbar);
-    }
-    if (tt == 0) {
-        qlen = 0;
-        nrun = 0;
-        rsum_t = 0;
-        fl[kp] = 0;
     }
     __syncthreads();
-    ptx::mbar_wait(tbar, 0);
-    mark(0);
 
-    unsigned long long sat = 0;
-    // Row sum of the final operand, kept incrementally (tier-1 words, tier-2
-    // corrections and extension pieces, plan_w copies) instead of a re-read pass.
     const bool want_rs = p.rowsum != nullptr;
-    int rs_run = 0;
-    // Row start: the team's previous bulk store has read fl / pk; zero the
-    // plan_x extension slots [K, C1); fetch the hot channels' x values.
-    auto row_begin = [&](int row) {
-        rs_run = 0;
-        if (tt == 0) ptx::bulk_wait_read_all();
-        team_sync<TW>(team);
-        const int z0 = (k + 15) & ~15;
-        if (z0 != k && tt == 0) *reinterpret_cast<uint2*>(fl + k) = make_uint2(0u, 0u);
-        for (int i = tt; i < (c1 - z0) >> 4; i += TW)
-            *reinterpret_cast<uint4*>(fl + z0 + 16 * i) = make_uint4(0u, 0u, 0u, 0u);
-    };
-    // ---- tier 1 on one chunk: one FFMA per element; tier-2 elements are queued ----
-    auto tier1 = [&](const uint4 (&buf)[kCh], int c) {
+    int rs[R];
 #pragma unroll
-        for (int i = 0; i < kCh; ++i) {
-            const int g = (c * kCh + i) * TW + tt;
-            if (g >= ng_all) break;
-            const float4 ca = reinterpret_cast<const float4*>(scj)[2 * g];
-            const float4 cb = reinterpret_cast<const float4*>(scj)[2 * g + 1];
-            const uint4 pw = reinterpret_cast<const uint4*>(spj)[g];
-            const float cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-            const uint32_t pv[4] = {pw.x, pw.y, pw.z, pw.w};
-            const uint4 xw = buf[i];
-            const uint32_t w[4] = {xw.x, xw.y, xw.z, xw.w};
+    for (int r = 0; r < R; ++r) rs[r] = 0;
+
+    // ---- 1. tier 1: one FFMA per element; tier-2 elements set a bitmap bit ----
+    const uint4* xr[R];  // row pointers (rows past M read row M - 1 and are never stored)
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        xr[r] = static_cast<const uint4*>(p.x) + static_cast<int64_t>(min(row0 + r, p.m - 1)) * (p.ldx >> 3);
+    const float4* const cj4 = reinterpret_cast<const float4*>(p.cj);
+    const uint4* const pj4 = reinterpret_cast<const uint4*>(p.pj);
+    for (int g = tid; g < ngrp; g += kThreads) {
+        uint4 xw[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) xw[r] = __ldg(xr[r] + g);
+        const float4 ca = __ldg(cj4 + 2 * g);
+        const float4 cb = __ldg(cj4 + 2 * g + 1);
+        const uint4 pw = __ldg(pj4 + g);
+        const float cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+        const uint32_t pv[4] = {pw.x, pw.y, pw.z, pw.w};
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t w[4] = {xw[r].x, xw[r].y, xw[r].z, xw[r].w};
             uint32_t tw[4], bq[8];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
@@ -357,165 +272,173 @@ __global__ void __launch_bounds__(kWarps * 32, 2) k_flatten16(const __grid_const
             }
             const uint32_t wlo = pack_lowbytes(bq[0], bq[1], bq[2], bq[3]);
             const uint32_t whi = pack_lowbytes(bq[4], bq[5], bq[6], bq[7]);
-            *reinterpret_cast<uint2*>(fl + 8 * g) = make_uint2(wlo, whi);
+            *reinterpret_cast<uint2*>(rows + r * ldf + 8 * g) = make_uint2(wlo, whi);
             if (want_rs) {
-                rs_run = __dp4a(static_cast<int>(wlo), 0x01010101, rs_run);
-                rs_run = __dp4a(static_cast<int>(whi), 0x01010101, rs_run);
-            }
-            if (const uint32_t hg = static_cast<uint32_t>(shotg[g]); (hg & 0xFFu) != 0u) {
-                uint32_t hm = hg & 0xFFu;  // hot channels of the group: keep their x for tier 2
-                int hi = static_cast<int>(hg >> 8);
-                while (hm != 0u) {
-                    const int e = __ffs(static_cast<int>(hm)) - 1;
-                    hm &= hm - 1u;
-                    const uint32_t wd = (e & 4) ? ((e & 2) ? xw.w : xw.z) : ((e & 2) ? xw.y : xw.x);
-                    hotx[hi++] = static_cast<uint16_t>(wd >> ((e & 1) << 4));
-                }
+                rs[r] = __dp4a(static_cast<int>(wlo), 0x01010101, rs[r]);
+                rs[r] = __dp4a(static_cast<int>(whi), 0x01010101, rs[r]);
             }
             const uint32_t all = tw[0] & tw[1] & tw[2] & tw[3] & 0x80008000u;
-            if (all != 0x80008000u) {
-                uint32_t msk = ((~tw[0] >> 15) & 1u) | ((~tw[0] >> 30) & 2u) |
-                               ((~tw[1] >> 13) & 4u) | ((~tw[1] >> 28) & 8u) |
-                               ((~tw[2] >> 11) & 16u) | ((~tw[2] >> 26) & 32u) |
-                               ((~tw[3] >> 9) & 64u) | ((~tw[3] >> 24) & 128u);
-                int slot = atomicAdd(&qlen, __popc(msk));
-                while (msk != 0u) {
-                    const int e = __ffs(static_cast<int>(msk)) - 1;
-                    msk &= msk - 1u;
-                    const uint32_t wd = (e & 4) ? ((e & 2) ? xw.w : xw.z) : ((e & 2) ? xw.y : xw.x);
-                    if (slot < kQCap)
-                        queue[slot] = make_uint2(static_cast<uint32_t>(8 * g + e),
-                                                 (wd >> ((e & 1) << 4)) & 0xFFFFu);
-                    ++slot;
-                }
+            if (all != 0x80008000u) {  // some element outside its certificate: tier 2
+                const uint32_t msk = ((~tw[0] >> 15) & 1u) | ((~tw[0] >> 30) & 2u) |
+                                     ((~tw[1] >> 13) & 4u) | ((~tw[1] >> 28) & 8u) |
+                                     ((~tw[2] >> 11) & 16u) | ((~tw[2] >> 26) & 32u) |
+                                     ((~tw[3] >> 9) & 64u) | ((~tw[3] >> 24) & 128u);
+                bitmap8[r * nbw * 4 + g] = static_cast<uint8_t>(msk);
             }
         }
-    };
-    auto exact = [&](int j, uint32_t xb, int cap_e, float rs32_j, int& ce, int& qe, int& fv) {
+    }
+    __syncthreads();
+
+    // ---- 2. exact splits: hot channels on every row, then the bitmap ----
+    unsigned long long sat = 0;
+    const uint16_t* x16 = static_cast<const uint16_t*>(p.x);
+    // piece 0 into slot j (replacing the tier-1 byte), pieces 1 .. E_j into the
+    // channel's extension slots; returns the change of the row sum
+    auto split_store = [&](int r, int j, int cap_e, int off_j, float rs32_j) -> int {
+        const uint32_t xb = __ldg(x16 + static_cast<int64_t>(row0 + r) * p.ldx + j);
         const float xf = mag_to_f32<F16>(xb & 0x7FFFu) * ((xb & 0x8000u) ? -1.0f : 1.0f);
         const uint64_t res = split_quant_elem(xf, static_cast<double>(xf), p.s + j, p.rs + j,
                                               rs32_j, cap_e, sc);
-        ce = static_cast<int>(res & 0xFFFF);
-        qe = static_cast<int>(static_cast<int16_t>(res >> 16));
-        fv = (res >> 32) & 1 ? -full : full;
+        const int ce = static_cast<int>(res & 0xFFFF);
+        const int qe = static_cast<int>(static_cast<int16_t>(res >> 16));
+        const int fv = (res >> 32) & 1 ? -sc.qT : sc.qT;
         sat += (res >> 33) & 1;
+        const int v0 = ce >= 1 ? fv : qe;
+        int8_t* fr = rows + r * ldf;
+        int d = v0 - fr[j];
+        fr[j] = static_cast<int8_t>(v0);
+        if (ce >= 1 && cap_e > 1) {
+            const int last = min(ce, cap_e - 1);
+            fill_pieces(fr + k + off_j, last, ce, fv, qe);
+            d += min(ce - 1, last) * fv + (ce <= last ? qe : 0);
+        }
+        return d;
     };
-    // Row end: tier 2, extension runs, plan_w copies, pack / sums, bulk store.
-    auto row_end = [&](int row) {
-        mark(1);
-        team_sync<TW>(team);
-        const int nq = qlen;
-        const bool overflow = nq > kQCap;
-        if (overflow) {  // pathological inputs: every non-hot tier-2 element inline
-            const uint16_t* xr = static_cast<const uint16_t*>(p.x) + static_cast<int64_t>(row) * p.ldx;
-            for (int j = tt; j < k; j += TW) {
-                const uint32_t xb = __ldg(xr + j);
-                if (spj[j] - (xb & 0x7FFFu) >= 0x8000u) continue;  // tier 1 or hot
-                int ce, qe, fv;
-                const int cap_e = __ldg(p.cap + j);
-                exact(j, xb, cap_e, __ldg(p.rs32 + j), ce, qe, fv);
-                const int v0 = ce >= 1 ? fv : qe;
-                if (want_rs) rs_run += v0 - fl[j];
-                fl[j] = static_cast<int8_t>(v0);
-                const int last = ce >= 1 ? min(ce, cap_e - 1) : 0;
-                fill_pieces(fl + k + __ldg(p.off + j), last, ce, fv, qe);
-                if (want_rs && ce >= 1) rs_run += min(ce - 1, last) * fv + (ce <= last ? qe : 0);
-            }
-        }
-        const int nitems = p.nhot + (overflow ? 0 : nq);
-        for (int i = tt; i < nitems; i += TW) {
-            int j, cap_e, off_j;
-            float rs32_j;
-            uint32_t xb;
-            if (i < p.nhot) {
-                const int4 hm = shot[i];
-                j = hm.x, cap_e = hm.y, off_j = hm.z, rs32_j = __int_as_float(hm.w);
-                xb = hotx[i];
-            } else {
-                const uint2 e = queue[i - p.nhot];
-                j = static_cast<int>(e.x);
-                xb = e.y;
-                cap_e = __ldg(p.cap + j), off_j = __ldg(p.off + j), rs32_j = __ldg(p.rs32 + j);
-            }
-            int ce, qe, fv;
-            exact(j, xb, cap_e, rs32_j, ce, qe, fv);
-            const int v0 = ce >= 1 ? fv : qe;
-            if (want_rs) rs_run += v0 - fl[j];  // tier 1 left its (replaced) byte in slot j
-            fl[j] = static_cast<int8_t>(v0);  // slot j = piece 0
-            if (ce >= 1) {  // pieces 1 .. E -> the (zeroed) extension slots
-                const int last = min(ce, cap_e - 1);
-                fill_pieces(fl + k + off_j, last, ce, fv, qe);
-                if (want_rs) rs_run += min(ce - 1, last) * fv + (ce <= last ? qe : 0);
-            }
-        }
-        team_sync<TW>(team);
-        mark(2);
-        if (tt == 0) qlen = 0, nrun = 0;
-        mark(3);
-        // plan_w copies [C1, K'): byte gathers from the flattened row
-#pragma unroll 4
-        for (int u = tt; u < ((kp - c1) >> 2); u += TW) {
-            const int4 sv = swsrc[u];
-            const uint32_t b0 = static_cast<uint8_t>(fl[sv.x]), b1 = static_cast<uint8_t>(fl[sv.y]);
-            const uint32_t b2 = static_cast<uint8_t>(fl[sv.z]), b3 = static_cast<uint8_t>(fl[sv.w]);
-            const uint32_t wv =
-                __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
-            *reinterpret_cast<uint32_t*>(fl + c1 + 4 * u) = wv;
-            if (want_rs) rs_run = __dp4a(static_cast<int>(wv), 0x01010101, rs_run);
-        }
-        if constexpr (PACK4) {  // byte i = q[i] & 15 | q[16 + i] << 4
-            team_sync<TW>(team);
-            for (int u = tt; u < (kp >> 5); u += TW) {
-                const uint4 lo = *reinterpret_cast<const uint4*>(fl + 32 * u);
-                const uint4 hi = *reinterpret_cast<const uint4*>(fl + 32 * u + 16);
-                *reinterpret_cast<uint4*>(pk + 16 * u) =
-                    make_uint4(pack_i4_word(lo.x, hi.x), pack_i4_word(lo.y, hi.y),
-                               pack_i4_word(lo.z, hi.z), pack_i4_word(lo.w, hi.w));
-            }
-        }
-        if (want_rs) {
-            int rsum = rs_run;
+    // the bitmap's elements as a dense list (ballot compaction, one SMEM atomic
+    // per warp), so the divergent exact path runs with full warps
+    for (int u0 = 0; u0 < nrow * nbw; u0 += kThreads) {
+        const int u = u0 + tid;
+        const uint32_t b = u < nrow * nbw ? bitmap[u] : 0u;
+        const int c = __popc(b);
+        int incl = c;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) rsum += __shfl_xor_sync(0xffffffffu, rsum, o);
-            if (lane == 0) atomicAdd(&rsum_t, rsum);
+        for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, o);
+            if ((tid & 31) >= o) incl += v;
         }
-        ptx::fence_proxy_async_smem();
-        team_sync<TW>(team);
-        mark(4);
-        if (tt == 0) {
-            ptx::bulk_store(p.q + static_cast<int64_t>(row) * p.ldq,
-                            PACK4 ? static_cast<const void*>(pk) : static_cast<const void*>(fl),
-                            PACK4 ? static_cast<uint32_t>(kp >> 1) : static_cast<uint32_t>(kp));
-            ptx::bulk_commit();
-            if (p.rowsum != nullptr) {
-                p.rowsum[row] = rsum_t;
-                rsum_t = 0;  // next use is after this team's next row_begin barrier
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        int base = 0;
+        if ((tid & 31) == 31 && total > 0) base = atomicAdd(&qlen, total);
+        base = __shfl_sync(0xffffffffu, base, 31) + incl - c;
+        if (c > 0) {
+            const int r = u / nbw, j0 = 32 * (u - r * nbw);
+            uint32_t bb = b;
+            while (bb != 0u) {
+                const int e = __ffs(static_cast<int>(bb)) - 1;
+                bb &= bb - 1u;
+                if (base < kListCap) list[base] = static_cast<uint32_t>(r << 24 | (j0 + e));
+                ++base;
             }
         }
-    };
-    auto step = [&](const uint4 (&buf)[kCh], int t) {
-        const int row = worker + (t / nch) * nworkers, c = t % nch;
-        if (c == 0) row_begin(row);
-        if (c == 0) mark(7);
-        tier1(buf, c);
-        if (c == nch - 1) row_end(row);
-    };
-
-    // software pipeline over this team's chunk stream: chunk t + 1 loads while t computes
-    for (int t = 0; t < nchunks; t += 2) {
-        load_chunk(xb, t + 1);
-        step(xa, t);
-        if (t + 1 >= nchunks) break;
-        load_chunk(xa, t + 2);
-        step(xb, t + 1);
     }
-    mark(5);
-    if (tt == 0) ptx::bulk_wait_all();
-    mark(6);
+    __syncthreads();
+    const int nhot_items = nrow * p.nhot;
+    const int nlist = min(qlen, kListCap);
+    for (int i = tid; i < nhot_items + nlist; i += kThreads) {
+        int r, j, cap_e, off_j;
+        float rs32_j;
+        if (i < nhot_items) {
+            r = i / p.nhot;
+            const int4 hm = __ldg(reinterpret_cast<const int4*>(p.hotm) + (i - r * p.nhot));
+            j = hm.x, cap_e = hm.y, off_j = hm.z, rs32_j = __int_as_float(hm.w);
+        } else {
+            const uint32_t e = list[i - nhot_items];
+            r = static_cast<int>(e >> 24), j = static_cast<int>(e & 0xFFFFFFu);
+            cap_e = __ldg(p.cap + j), off_j = __ldg(p.off + j), rs32_j = __ldg(p.rs32 + j);
+        }
+        const int d = split_store(r, j, cap_e, off_j, rs32_j);
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) rs[rr] += rr == r ? d : 0;
+    }
+    if (qlen > kListCap) {  // pathological input: the rest, straight from the bitmap
+        for (int u = tid; u < nrow * nbw; u += kThreads) {
+            uint32_t b = bitmap[u];
+            const int r = u / nbw, j0 = 32 * (u - r * nbw);
+            int dsum = 0;
+            while (b != 0u) {
+                const int e = __ffs(static_cast<int>(b)) - 1;
+                b &= b - 1u;
+                const int j = j0 + e;
+                bool listed = false;  // the first kListCap entries were processed above
+                for (int q = 0; q < kListCap && !listed; ++q)
+                    listed = list[q] == static_cast<uint32_t>(r << 24 | j);
+                if (!listed)
+                    dsum += split_store(r, j, __ldg(p.cap + j), __ldg(p.off + j), __ldg(p.rs32 + j));
+            }
+#pragma unroll
+            for (int rr = 0; rr < R; ++rr) rs[rr] += rr == r ? dsum : 0;
+        }
+    }
+    __syncthreads();
+
+    // ---- 3. plan_w copies [C1, K') ----
+    for (int u = tid; u < ((kp - c1) >> 2); u += kThreads) {
+        const int4 sv = __ldg(reinterpret_cast<const int4*>(p.wsrc) + u);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint8_t* fr = reinterpret_cast<const uint8_t*>(rows + r * ldf);
+            const uint32_t wv =
+                static_cast<uint32_t>(fr[sv.x]) | (static_cast<uint32_t>(fr[sv.y]) << 8) |
+                (static_cast<uint32_t>(fr[sv.z]) << 16) | (static_cast<uint32_t>(fr[sv.w]) << 24);
+            *reinterpret_cast<uint32_t*>(rows + r * ldf + c1 + 4 * u) = wv;
+            if (want_rs) rs[r] = __dp4a(static_cast<int>(wv), 0x01010101, rs[r]);
+        }
+    }
+    if (want_rs) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            int v = rs[r];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if ((tid & 31) == 0 && v != 0) atomicAdd(&rsum_s[r], v);
+        }
+    }
+    __syncthreads();
+
+    // ---- 4. int4 packing in place, then one bulk copy per row ----
+    if constexpr (PACK4) {  // byte i = q[i] & 15 | q[16 + i] << 4 per group of 32
+        // group u reads bytes [32u, 32u + 32) and writes [16u, 16u + 16): a barrier
+        // between the reads and the writes of each pass keeps it race-free
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            int8_t* fr = rows + r * ldf;
+            for (int u0 = 0; u0 < (kp >> 5); u0 += kThreads) {
+                const int u = u0 + tid;
+                uint4 o = make_uint4(0u, 0u, 0u, 0u);
+                if (u < (kp >> 5)) {
+                    const uint4 lo = *reinterpret_cast<const uint4*>(fr + 32 * u);
+                    const uint4 hi = *reinterpret_cast<const uint4*>(fr + 32 * u + 16);
+                    o = make_uint4(pack_i4_word(lo.x, hi.x), pack_i4_word(lo.y, hi.y),
+                                   pack_i4_word(lo.z, hi.z), pack_i4_word(lo.w, hi.w));
+                }
+                __syncthreads();
+                if (u < (kp >> 5)) *reinterpret_cast<uint4*>(fr + 16 * u) = o;
+            }
+        }
+    }
+    ptx::fence_proxy_async_smem();  // generic-proxy SMEM writes -> visible to the bulk copies
+    __syncthreads();
+    if (tid < nrow) {
+        ptx::bulk_store(p.q + static_cast<int64_t>(row0 + tid) * p.ldq, rows + tid * ldf,
+                        PACK4 ? static_cast<uint32_t>(kp >> 1) : static_cast<uint32_t>(kp));
+        ptx::bulk_commit();
+        if (want_rs) p.rowsum[row0 + tid] = rsum_s[tid];
+    }
     if (p.sat != nullptr) {
         sat = warp_sum(sat);
-        if (lane == 0 && sat) atomicAdd(p.sat, sat);
+        if ((tid & 31) == 0 && sat) atomicAdd(p.sat, sat);
     }
+    if (tid < nrow) ptx::bulk_wait_all();
 }
 
 }  // namespace
@@ -529,18 +452,28 @@ void tier1_tables(const double* s, int64_t k, double act_scale, double t, double
 }
 
 bool flatten16(const FlattenArgs& a, cudaStream_t st) {
-    if (a.cj == nullptr || a.pj == nullptr || a.wsrc16 == nullptr || a.hotg == nullptr ||
-        a.amax != nullptr)
+    if (a.cj == nullptr || a.pj == nullptr || a.wsrc16 == nullptr || a.amax != nullptr)
         return false;
     if (a.x_dtype != FQG_BF16 && a.x_dtype != FQG_F16) return false;
     if (a.k % 8 != 0 || a.k >= (1 << 24) || a.ldx % 8 != 0 || a.nhot > kMaxHot ||
         reinterpret_cast<uintptr_t>(a.x) % 16 != 0)
         return false;
     if (reinterpret_cast<uintptr_t>(a.q) % 16 != 0 || a.ldq % 16 != 0) return false;
-    constexpr int TW = 32;  // threads per row team
-    const K1Smem w = k1_smem(static_cast<int>(a.k), static_cast<int>(a.kp), static_cast<int>(a.c1),
-                             a.pack4, kWarps * 32 / TW);
-    if (w.total > 220 * 1024) return false;
+    // rows per block: the largest of 8/4/2/1 that still gives >= 3 blocks per SM
+    int rb = 8;
+    while (rb > 1 && (a.m + rb - 1) / rb < 3 * a.num_sms) rb >>= 1;
+    static const int rb_env = [] {  // tuning override: FQG_K1_ROWS = 1, 2, 4 or 8
+        const char* e = std::getenv("FQG_K1_ROWS");
+        return e ? std::atoi(e) : 0;
+    }();
+    if (rb_env == 1 || rb_env == 2 || rb_env == 4 || rb_env == 8) rb = rb_env;
+    const int ldf = static_cast<int>((a.kp + 16 + 15) / 16 * 16);
+    auto smem_of = [&](int r) {
+        return static_cast<size_t>(r) * ldf + static_cast<size_t>(r) * ((a.k / 8 + 3) / 4) * 4;
+    };
+    while (rb > 1 && smem_of(rb) > 200 * 1024) rb >>= 1;
+    const size_t smem = smem_of(rb);
+    if (smem > 220 * 1024) return false;
     K16Params p{};
     p.x = a.x;
     p.ldx = a.ldx;
@@ -548,23 +481,17 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     p.k = static_cast<int>(a.k);
     p.kp = static_cast<int>(a.kp);
     p.c1 = static_cast<int>(a.c1);
-    p.ldf = w.ldf;
+    p.ldf = ldf;
     p.nhot = static_cast<int>(a.nhot);
-    p.s_cj = w.cj, p.s_pj = w.pj, p.s_wsrc = w.wsrc, p.s_hotm = w.hotm, p.per_team0 = w.per_team0;
-    p.s_hotg = w.hotg, p.s_tbar = w.tbar, p.hotg_bytes = w.hotg_bytes;
-    p.hotm = a.hotm;
-    p.hotg = a.hotg;
-    p.fl = w.fl, p.pk = w.pk, p.queue = w.queue, p.runs = w.runs, p.hotx = w.hotx;
-    p.per_team = w.per_team;
     p.cj = a.cj;
     p.pj = a.pj;
-    p.hot = a.hot;
+    p.hotm = a.hotm;
     p.off = a.off;
     p.wsrc = a.wsrc16;
     p.s = a.s;
     p.rs = a.rs;
-    p.rs32 = a.rs32;
     p.cap = a.cap;
+    p.rs32 = a.rs32;
     {  // SplitConsts on the host: the same IEEE double arithmetic as make_consts
         SplitConsts& c = p.sc;
         c.t = a.t;
@@ -583,48 +510,34 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     p.ldq = a.ldq;
     p.sat = a.sat;
     p.rowsum = a.rowsum;
-    static const int dbg = [] {
-        const char* e = std::getenv("FQG_K1_DEBUG");
-        return e ? std::atoi(e) : 0;
-    }();
-    p.dbg = dbg;
-    if (dbg) {
-        static unsigned long long zeros[16] = {};
-        FQG_CUDA(cudaMemcpyToSymbol(g_k1dbg, zeros, sizeof(zeros)));
-    }
-    auto run = [&](auto kern) {
-        FQG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(w.total)));
-        int occ = 0;
-        FQG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kWarps * 32, w.total));
-        constexpr int teams = kWarps * 32 / TW;
-        const int64_t ctas_needed = (a.m + teams - 1) / teams;
-        const int grid = static_cast<int>(
-            std::max<int64_t>(1, std::min<int64_t>(ctas_needed, std::max(1, occ) * a.num_sms)));
-        kern<<<grid, kWarps * 32, w.total, st>>>(p);
-        FQG_CUDA(cudaGetLastError());
-        if (dbg) {
-            unsigned long long h[16];
-            FQG_CUDA(cudaDeviceSynchronize());
-            FQG_CUDA(cudaMemcpyFromSymbol(h, g_k1dbg, sizeof(h)));
-            const double nt = static_cast<double>(grid) * (kWarps * 32 / TW);  // team leaders
-            std::fprintf(stderr,
-                         "[fqg k1] avg cycles since start per team: staged %.0f, row_begin done "
-                         "%.0f, tier1 done %.0f, tier2 done %.0f, runs done %.0f, copies done %.0f, "
-                         "loop end %.0f, stores done %.0f (grid %d)\n",
-                         h[0] / nt, h[7] / nt, h[1] / nt, h[2] / nt, h[3] / nt, h[4] / nt,
-                         h[5] / nt, h[6] / nt, grid);
+    const bool f16 = a.x_dtype == FQG_F16;
+    const unsigned grid = static_cast<unsigned>((a.m + rb - 1) / rb);
+    auto go = [&](auto rc) {
+        constexpr int R = decltype(rc)::value;
+        auto run = [&](auto kern) {
+            kern<<<grid, kThreads, smem, st>>>(p);
+            FQG_CUDA(cudaGetLastError());
+        };
+        if (f16 && a.pack4) {
+            ensure_smem_attr<k_flatten16<true, true, R>>(220 * 1024);
+            run(k_flatten16<true, true, R>);
+        } else if (f16) {
+            ensure_smem_attr<k_flatten16<true, false, R>>(220 * 1024);
+            run(k_flatten16<true, false, R>);
+        } else if (a.pack4) {
+            ensure_smem_attr<k_flatten16<false, true, R>>(220 * 1024);
+            run(k_flatten16<false, true, R>);
+        } else {
+            ensure_smem_attr<k_flatten16<false, false, R>>(220 * 1024);
+            run(k_flatten16<false, false, R>);
         }
     };
-    const bool f16 = a.x_dtype == FQG_F16;
-    if (f16 && a.pack4)
-        run(k_flatten16<true, true, TW>);
-    else if (f16)
-        run(k_flatten16<true, false, TW>);
-    else if (a.pack4)
-        run(k_flatten16<false, true, TW>);
-    else
-        run(k_flatten16<false, false, TW>);
+    switch (rb) {
+        case 8: go(std::integral_constant<int, 8>{}); break;
+        case 4: go(std::integral_constant<int, 4>{}); break;
+        case 2: go(std::integral_constant<int, 2>{}); break;
+        default: go(std::integral_constant<int, 1>{}); break;
+    }
     return true;
 }
 

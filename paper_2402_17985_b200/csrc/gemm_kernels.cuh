@@ -748,7 +748,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             // 2-byte outputs, no bias, full tile: 16-column chunks with the next
             // chunk's TMEM load in flight while this one is converted and stored
             constexpr bool OUT16 = OUT == FQG_F16 || OUT == FQG_BF16;
-            if (OUT16 && !plane && bias == nullptr && vec_ok && !(dbg & 12) &&
+            if (OUT16 && !plane && bias == nullptr && (vec_ok & 2) && !(dbg & 12) &&
                 (n_blk + 1) * TN <= n) {
                 const int mode = cvt_mode(small_acc, s32);
                 constexpr int NCH = TN / 16;
@@ -1135,6 +1135,8 @@ void launch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t stream) {
     FQG_CUDA(cudaGetDevice(&dev));
     const int esz = dtype_size(g.y_dtype);
     const bool vec = (reinterpret_cast<uintptr_t>(g.y) % 16 == 0) && ((g.ldy * esz) % 16 == 0);
+    // 32-byte row stores (st.global.v8) of the 16-column drain need 32-byte rows
+    const bool vec32 = (reinterpret_cast<uintptr_t>(g.y) % 32 == 0) && ((g.ldy * esz) % 32 == 0);
     const int num_kb = static_cast<int>((g.kp + BK - 1) / BK);
     static const int dbg = [] {
         const char* e = std::getenv("FQG_GEMM_DEBUG");
@@ -1184,7 +1186,8 @@ void launch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t stream) {
     cfg.numAttrs = pdl ? 1 : 0;
     cudaError_t le = cudaLaunchKernelEx(
         &cfg, kern, ta, tb, g.y, g.ldy, static_cast<int>(g.m), static_cast<int>(g.n), num_kb,
-        g.scale, g.bias, g.bias_dtype, vec ? 1 : 0, dbg, g.rowsum, sk, ws, ty, tma_y ? 1 : 0,
+        g.scale, g.bias, g.bias_dtype, (vec ? 1 : 0) | (vec32 ? 2 : 0), dbg, g.rowsum, sk, ws, ty,
+        tma_y ? 1 : 0,
         small_acc(g) ? 1 : 0);
     if (le == cudaSuccess) le = cudaGetLastError();
     if (le == cudaSuccess && sk >= 2) {

@@ -247,6 +247,7 @@ fqg_layer_s* create(const fqg_layer_desc& d) {
             }
             upload(L->d_hotm, hotm);
             upload(L->d_hotg, hotg);
+
             std::vector<uint16_t> pj(static_cast<size_t>(d.k));
             for (int f = 0; f < 2 && !hot.empty(); ++f) {
                 FQG_CUDA(cudaMemcpy(pj.data(), L->d_pj[f].p, pj.size() * 2, cudaMemcpyDeviceToHost));
