@@ -11,8 +11,16 @@ epilogue to fp16 (K4) over one batch; inputs resident in HBM, L2 flushed
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 
-N>1 (torchrun): the layer is N-sharded over ranks (global s_w), each rank runs
-its column shard, outputs are all-gathered with NCCL; scaling "strong".
+N > 1: run under torchrun (or let --gpus N re-launch this script under
+torch.distributed.run itself). The layer is N-sharded over the ranks (global
+s_w): each rank runs K1 on the replicated input and K4 on its column shard,
+writing straight into its slot of a shard-major buffer, and the slots are
+all-gathered in place with NCCL; scaling "strong" (fixed total work), timed as
+the max over ranks.
+
+At N = 1 the line also carries `subresults` for the other BASELINE configs
+(configs[0], [2], [3] one-GPU shards, [4] M sweep), each with value, ms, the
+K1/K4 split and the K4 roofline fraction (--no-subresults skips them).
 """
 from __future__ import annotations
 
@@ -20,6 +28,7 @@ import argparse
 import ctypes
 import json
 import os
+import socket
 import subprocess
 import sys
 import time
@@ -37,6 +46,9 @@ CONFIGS = {
     "llama13b_up": (5120, 13824, 2048, 4),     # configs[3]
     "sweep_8192": (8192, 8192, 8192, 8),       # configs[4] largest point
 }
+OPT67B = [("qkv", 4096, 12288, 4), ("o", 4096, 4096, 8), ("fc1", 4096, 16384, 4),
+          ("fc2", 16384, 4096, 8)]                  # configs[2], M = 2048
+SWEEP_M = [1, 16, 128, 256, 512, 1024, 2048, 4096, 8192]  # configs[4]
 SPEC_INT8_TOPS = 4500.0
 
 
@@ -71,7 +83,7 @@ class Clocks:
         try:
             self.p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except Exception:
             self.p = None
@@ -114,22 +126,28 @@ def dist_env():
     return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
 
 
-from paper_2402_17985_b200.shard import gather_columns, shard_bounds  # noqa: E402
+def relaunch_distributed(nproc: int) -> int:
+    """--gpus N outside torchrun: re-run this script under torch.distributed.run."""
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nproc}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
 
 
-def cpu_reference_sample(k, n, bits, rows, threads, steps=1, warmup=0, recipe_layer=None):
-    """Times the UNMODIFIED reference fq::run_layer (oracle/_ref), row-parallel
-    over `threads` host threads, on a bounded row sample of the workload."""
-    from oracle import Ref
+from paper_2402_17985_b200.shard import shard_bounds, shard_width  # noqa: E402
 
-    ref = Ref()
-    w, calib, x, _ = ref.synthetic_layer(0, in_channels=k, out_channels=n, rows=32, samples=4)
-    if recipe_layer is None:
-        rl = ref.quantize_layer(w, calib, mode=1 if bits == 8 else 2,
-                                gamma=1.86 if bits == 8 else 1e6)
-    else:
-        rl = ref.layer_from(recipe_layer)
-    xs = np.ascontiguousarray(np.tile(x, (-(-rows // x.shape[0]), 1))[:rows])
+
+def reference_recipe(ref, w, calib, bits):
+    """The reference's own fq::quantize_layer (O1 INT8 / O2 forced INT4)."""
+    return ref.quantize_layer(w, calib, mode=1 if bits == 8 else 2,
+                              gamma=1.86 if bits == 8 else 1e6)
+
+
+def time_reference(rl, xs, threads, steps=1, warmup=0):
     for _ in range(warmup):
         rl.run_layer(xs, nthreads=threads)
     ts = []
@@ -137,38 +155,245 @@ def cpu_reference_sample(k, n, bits, rows, threads, steps=1, warmup=0, recipe_la
         t0 = time.perf_counter()
         rl.run_layer(xs, nthreads=threads)
         ts.append(time.perf_counter() - t0)
-    kp = rl.info.Kp
-    t = float(np.mean(ts))
-    return {"rows": rows, "seconds": t, "tops": 2.0 * rows * n * kp / t / 1e12,
-            "tokens_per_s": rows / t, "kp": kp}
+    return float(np.mean(ts))
 
 
 def run_reference_arm(args):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified
+    fq_core compiled from /root/reference sources) on the same synthetic input
+    rows as the GPU arm, row-parallel over all host threads."""
     rank, _, world = dist_env()
     if rank != 0:
         return 0
+    from oracle import Ref
+
+    import paper_2402_17985_b200 as fq  # host-only: the synthetic generator
+
     k, n, m, bits = CONFIGS[args.config]
     threads = os.cpu_count() or 1
-    res = cpu_reference_sample(k, n, bits, rows=args.cpu_rows or m, threads=threads,
-                               steps=args.steps, warmup=max(0, min(args.warmup, 1)))
+    ref = Ref()
+    w, calib, x = fq.synthetic_layer(0, test_rows=m, in_channels=k, out_channels=n, rows=32,
+                                     samples=4)
+    xs = bf16_round(x)
+    rows = args.cpu_rows or m
+    xs = np.ascontiguousarray(xs[:rows])
+    rl = reference_recipe(ref, w, calib, bits)
+    t = time_reference(rl, xs, threads, steps=args.steps, warmup=max(0, min(args.warmup, 1)))
+    kp = rl.info.Kp
+    tops = 2.0 * rows * n * kp / t / 1e12
     line = {
-        "impl": "reference", "metric": METRIC, "value": res["tops"], "unit": "TOPS",
-        "tokens_per_s": res["tokens_per_s"], "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": res["seconds"] * 1e3, "higher_is_better": True,
+        "impl": "reference", "metric": METRIC, "value": tops, "unit": "TOPS",
+        "tokens_per_s": rows / t, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64 (int64 GEMM)", "data": "synthetic",
-        "config": {"workload": args.config, "K": k, "N": n, "M": m, "bits": bits,
-                   "Kp": res["kp"], "parallelism": "host threads"},
-        "cpu_baseline": {"value": res["tops"], "unit": "TOPS", "cores": threads,
-                         "kind": "reference",
-                         "sample": f"{res['rows']} rows of the M={m} workload per step, "
-                                   f"fq::run_layer row-parallel ({threads} threads), "
-                                   "recipe from fq::quantize_layer"},
-        "e2e": {"value": res["tops"], "unit": "TOPS", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+        "config": {"workload": args.config, "K": k, "N": n, "M": m, "bits": bits, "Kp": kp,
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": tops, "unit": "TOPS", "cores": threads, "kind": "reference",
+                         "sample": f"{rows} rows of the M={m} workload per step (the GPU arm's "
+                                   f"synthetic rows, bf16-rounded), fq::run_layer row-parallel "
+                                   f"({threads} threads), recipe from fq::quantize_layer"},
+        "e2e": {"value": tops, "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def bf16_round(x):
+    import torch
+
+    return torch.from_numpy(np.ascontiguousarray(x)).to(torch.bfloat16).double().numpy()
+
+
+class LayerBench:
+    """K1 + K4 of one layer replayed from CUDA graphs: the step graph (K1, then K4
+    as a programmatic dependent launch) and K1 / K4 graphs of their own for the
+    split. L2 flushed (256 MiB write) before every timed replay."""
+
+    def __init__(self, fq, layer, xt, out=None, flush=None):
+        import torch
+
+        self.fq, self.layer, self.xt = fq, layer, xt
+        m = xt.shape[0]
+        self.m = m
+        kp = layer.kp
+        ldq = kp // 2 if layer.info.a_format == fq.I4 else kp
+        dev = xt.device
+        self.q = torch.empty((m, ldq), dtype=torch.int8, device=dev)
+        self.rowsum = torch.empty(m, dtype=torch.int32, device=dev)
+        self.sat = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.y = out if out is not None else torch.empty((m, layer.n), dtype=torch.float16,
+                                                         device=dev)
+        self.flush = flush if flush is not None else torch.empty(256 << 20, dtype=torch.uint8,
+                                                                 device=dev)
+        self.graphs = None
+        self.k1_runs = 0  # K1 executions (the saturation counter accumulates over all)
+
+    def k1(self):
+        import torch
+
+        self.k1_runs += 1
+        self.fq.check(self.fq.lib().fqg_layer_quantize_acts_ex(
+            self.layer._h, self.xt.data_ptr(), self.fq.BF16, self.m, self.q.data_ptr(),
+            self.rowsum.data_ptr(), self.sat.data_ptr(), torch.cuda.current_stream().cuda_stream))
+
+    def k4(self):
+        import torch
+
+        self.fq.check(self.fq.lib().fqg_layer_gemm_ex(
+            self.layer._h, self.q.data_ptr(), self.rowsum.data_ptr(), self.m, self.y.data_ptr(),
+            self.fq.F16, self.y.stride(0), None, self.fq.NONE,
+            torch.cuda.current_stream().cuda_stream))
+
+    def capture(self, warmup):
+        import torch
+
+        for _ in range(warmup):
+            self.k1()
+            self.k4()
+        torch.cuda.synchronize()
+        g1, g4, gs = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g1):
+            self.k1()
+        with torch.cuda.graph(g4):
+            self.k4()
+        with torch.cuda.graph(gs):
+            self.k1()
+            self.k4()
+        self.k1_runs -= 3  # the captures did not execute
+        for _ in range(2):
+            g1.replay()
+            g4.replay()
+            gs.replay()
+        self.k1_runs += 4
+        torch.cuda.synchronize()
+        self.graphs = (g1, g4, gs)
+
+    def time(self, steps, after_step=None):
+        """(t_step, t_k1, t_k4, t_after) in ms, means over `steps` flushed replays."""
+        import torch
+
+        g1, g4, gs = self.graphs
+        E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        ev = [(E(), E(), E()) for _ in range(steps)]
+        for i in range(steps):
+            self.flush.fill_(i & 255)
+            ev[i][0].record()
+            gs.replay()
+            ev[i][1].record()
+            if after_step is not None:
+                after_step()
+            ev[i][2].record()
+        sp = [(E(), E(), E()) for _ in range(steps)]
+        for i in range(steps):
+            self.flush.fill_(i & 255)
+            sp[i][0].record()
+            g1.replay()
+            sp[i][1].record()
+            g4.replay()
+            sp[i][2].record()
+        torch.cuda.synchronize()
+        self.k1_runs += 2 * steps
+        mean = lambda v: float(sum(v) / len(v))  # noqa: E731
+        return (mean([a.elapsed_time(b) for a, b, _ in ev]),
+                mean([a.elapsed_time(b) for a, b, _ in sp]),
+                mean([b.elapsed_time(c) for _, b, c in sp]),
+                mean([b.elapsed_time(c) for _, b, c in ev]))
+
+
+def layer_result(fq, cfg, k, n, m, bits, x, steps, warmup, i8_peak, n_begin=0, n_cols=None,
+                 flush=None):
+    """One layer's bench entry (value, ms, K1/K4 split, K4 roofline fraction)."""
+    import torch
+
+    b_fmt = fq.I4 if bits == 4 else fq.I8
+    n_cols = n if n_cols is None else n_cols
+    layer = fq.Layer(cfg, a_format=fq.I8, b_format=b_fmt, n_begin=n_begin, n=n_cols)
+    xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    lb = LayerBench(fq, layer, xt, flush=flush)
+    lb.capture(warmup)
+    t_step, t_k1, t_k4, _ = lb.time(steps)
+    ops = 2.0 * m * n_cols * layer.kp
+    res = {"K": k, "N": n_cols, "M": m, "bits": bits, "Kp": layer.kp,
+           "value": ops / (t_step * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": t_step,
+           "tokens_per_s": m / (t_step * 1e-3),
+           "breakdown_ms": {"flatten_quant_K1": t_k1, "gemm_K4": t_k4, "K1_K4_graph": t_step},
+           "roofline_frac_K4": ops / (t_k4 * 1e-3) / 1e12 / i8_peak}
+    del lb, layer, xt
+    torch.cuda.empty_cache()
+    return res
+
+
+def subresults(fq, args, i8_peak, flush):
+    """configs[0], [2], [3] (one-GPU shards), [4] at N = 1."""
+    out = {}
+    k, n, m, bits = CONFIGS["w8a8_4096_m256"]
+    w, calib, x = fq.synthetic_layer(0, test_rows=m, in_channels=k, out_channels=n, rows=32,
+                                     samples=4)
+    cfg = fq.quantize_layer(w, calib, bits)
+    out["configs[0] w8a8_4096_m256"] = layer_result(fq, cfg, k, n, m, bits, bf16_round(x), 20,
+                                                    5, i8_peak, flush=flush)
+    opt, tot_ops, tot_t = {}, 0.0, 0.0
+    for i, (name, k, n, bits) in enumerate(OPT67B):
+        w, calib, x = fq.synthetic_layer(i + 1, test_rows=2048, in_channels=k, out_channels=n,
+                                         rows=32, samples=4)
+        cfg = fq.quantize_layer(w, calib, bits)
+        r = layer_result(fq, cfg, k, n, 2048, bits, bf16_round(x), 10, 3, i8_peak, flush=flush)
+        opt[name] = r
+        tot_ops += r["value"] * r["ms_per_step"] * 1e9
+        tot_t += r["ms_per_step"]
+    out["configs[2] opt6.7b_m2048"] = {"layers": opt, "value": tot_ops / (tot_t * 1e-3) / 1e12,
+                                       "unit": "TOPS", "ms_per_block": tot_t,
+                                       "bits": "qkv/fc1 4-bit, o/fc2 8-bit (pinned)"}
+    k, n, m, bits = CONFIGS["llama13b_up"]
+    w, calib, x = fq.synthetic_layer(13, test_rows=m, in_channels=k, out_channels=n, rows=32,
+                                     samples=4)
+    cfg = fq.quantize_layer(w, calib, bits)
+    xb = bf16_round(x)
+    ll = {}
+    for world in (1, 2, 4, 8):
+        b0, b1 = shard_bounds(n, world, 0)
+        ll[f"shard_of_{world}"] = layer_result(fq, cfg, k, n, m, bits, xb, 10, 3, i8_peak,
+                                               n_begin=b0, n_cols=b1 - b0, flush=flush)
+    out["configs[3] llama13b_up_m2048 (per-GPU shard, no collective)"] = ll
+    k, n, _, bits = CONFIGS["sweep_8192"]
+    w, calib, x = fq.synthetic_layer(21, test_rows=max(SWEEP_M), in_channels=k, out_channels=n,
+                                     rows=32, samples=4)
+    cfg = fq.quantize_layer(w, calib, bits)
+    xb = bf16_round(x)
+    sw = {}
+    for m in SWEEP_M:
+        sw[f"M={m}"] = layer_result(fq, cfg, k, n, m, bits, np.ascontiguousarray(xb[:m]),
+                                    10 if m >= 1024 else 20, 3, i8_peak, flush=flush)
+    out["configs[4] sweep_8192_int8"] = sw
+    return out
+
+
+def cpu_baseline(fq, cfg, layer, x, bits, k, n, m):
+    """The unmodified reference fq::run_layer (oracle/_ref) on the same recipe and
+    rows: all host threads on the full batch, and one thread on a row sample."""
+    from oracle import Layer as OLayer
+    from oracle import Ref
+
+    ref = Ref()
+    rec = OLayer(bits=bits, s=cfg.smooth_scales, t_x=cfg.plan_x.threshold,
+                 e_x=cfg.plan_x.extensions, t_w=cfg.plan_w.threshold, e_w=cfg.plan_w.extensions,
+                 wq=layer.weight_q(), s_w=layer.w_scale, act_scale=cfg.act_scale)
+    rl = ref.layer_from(rec)
+    threads = os.cpu_count() or 1
+    t_all = time_reference(rl, np.ascontiguousarray(x), threads)
+    rows1 = 16
+    t_one = time_reference(rl, np.ascontiguousarray(x[:rows1]), 1)
+    kp = layer.kp
+    return {
+        "value": 2.0 * m * n * kp / t_all / 1e12, "unit": "TOPS", "cores": threads,
+        "kind": "reference", "tokens_per_s": m / t_all,
+        "sample": f"{m} rows of the same layer/recipe, unmodified fq::run_layer (oracle/_ref) "
+                  f"row-parallel on {threads} host threads, {t_all:.2f} s",
+        "single_thread": {"value": 2.0 * rows1 * n * kp / t_one / 1e12, "unit": "TOPS",
+                          "tokens_per_s": rows1 / t_one, "cores": 1,
+                          "sample": f"{rows1} rows, one thread, {t_one:.2f} s"},
+    }
 
 
 def main():
@@ -181,19 +406,25 @@ def main():
     ap.add_argument("--a-format", default="auto", choices=["auto", "i8", "i4"])
     ap.add_argument("--b-format", default="auto", choices=["auto", "i8", "i4"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-subresults", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=0, help="CPU sample rows (0: the full M)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--chunks", type=int, default=1, help="N > 1: GEMM/all-gather M-chunks")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    rank, local_rank, world = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return relaunch_distributed(args.gpus)
     if args.impl == "reference":
         return run_reference_arm(args)
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     import torch
     import torch.distributed as dist
 
     import paper_2402_17985_b200 as fq
 
-    rank, local_rank, world = dist_env()
     torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
@@ -214,122 +445,78 @@ def main():
                                      samples=4)
     cfg = fq.quantize_layer(w, calib, bits)
     b0, b1 = shard_bounds(n, world, rank)
+    width = shard_width(n, world)
     layer = fq.Layer(cfg, device=local_rank, a_format=a_fmt, b_format=b_fmt, n_begin=b0,
                      n=b1 - b0)
     kp = layer.kp
-    xt = torch.from_numpy(x).to(torch.bfloat16).to(f"cuda:{local_rank}")
-    ldq = kp // 2 if a_fmt == fq.I4 else kp
-    q = torch.empty((m, ldq), dtype=torch.int8, device=xt.device)
-    y = torch.empty((m, b1 - b0), dtype=torch.float16, device=xt.device)
-    rowsum = torch.empty(m, dtype=torch.int32, device=xt.device)  # K1 -> K4 (biased int4 weights)
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device=xt.device)
-    cur = lambda: torch.cuda.current_stream().cuda_stream  # noqa: E731 (capture-aware)
-
-    def k1():
-        fq.check(fq.lib().fqg_layer_quantize_acts_ex(layer._h, xt.data_ptr(), fq.BF16, m,
-                                                     q.data_ptr(), rowsum.data_ptr(), None, cur()))
-
-    def k4():
-        fq.check(fq.lib().fqg_layer_gemm_ex(layer._h, q.data_ptr(), rowsum.data_ptr(), m,
-                                            y.data_ptr(), fq.F16, y.stride(0), None, fq.NONE,
-                                            cur()))
+    dev = torch.device("cuda", local_rank)
+    xt = torch.from_numpy(x).to(torch.bfloat16).to(dev)
+    # shard-major output [world][M][width]: this rank's K4 writes its slot, the
+    # all-gather fills the others in place (no reassembly copy)
+    gbuf = torch.empty((world, m, width), dtype=torch.float16, device=dev)
+    slot = gbuf[rank, :, : b1 - b0]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    lb = LayerBench(fq, layer, xt, out=slot, flush=flush)
 
     def gather():
         if world > 1:
-            gather_columns(y, n)  # NCCL all-gather of the column shards -> [M, N]
+            dist.all_gather_into_tensor(gbuf.view(world * m, width), gbuf[rank])
 
     for _ in range(args.warmup):
-        k1()
-        k4()
         gather()
-    torch.cuda.synchronize()
+    lb.capture(args.warmup)
     barrier()
-    # K1 and K4 are replayed from CUDA graphs (captured once after warm-up), so
-    # the timed region measures the device, not the Python/ctypes launch path.
-    # g_step holds K1 -> K4 as one graph: K4 is a programmatic dependent launch
-    # (its prologue overlaps K1's tail); g_k1 / g_k4 time the kernels apart.
-    g_k1, g_k4, g_step = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g_k1):
-        k1()
-    with torch.cuda.graph(g_k4):
-        k4()
-    with torch.cuda.graph(g_step):
-        k1()
-        k4()
-    for _ in range(2):
-        g_k1.replay()
-        g_k4.replay()
-        g_step.replay()
-    torch.cuda.synchronize()
-
-    E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-    evs = [(E(), E(), E(), E()) for _ in range(args.steps)]
-    evs_step = [(E(), E()) for _ in range(args.steps)]
     with Clocks(local_rank) as clk:
         torch.cuda.synchronize()
         barrier()
-        for i in range(args.steps):
-            flush.fill_(i & 255)
-            evs_step[i][0].record()
-            g_step.replay()
-            evs_step[i][1].record()
-            gather()
+        t_k1k4, t_k1, t_k4, t_ag = lb.time(args.steps, after_step=gather if world > 1 else None)
         torch.cuda.synchronize()
         barrier()
-        for i in range(args.steps):
-            flush.fill_(i & 255)  # evict L2 between timed steps (not timed)
-            e0, e1, e2, e3 = evs[i]
-            e0.record()
-            g_k1.replay()
-            e1.record()
-            g_k4.replay()
-            e2.record()
-            gather()
-            e3.record()
-        torch.cuda.synchronize()
-        barrier()
-    launches_per_step = 2 + (1 if m <= 512 else 0)  # + split-K reduce for small M
-    t_k1 = sum(a.elapsed_time(b) for a, b, _, _ in evs) / args.steps
-    t_k4 = sum(b.elapsed_time(c) for _, b, c, _ in evs) / args.steps
-    # no collective at N = 1 (the empty e2 -> e3 pair only measures event overhead)
-    t_ag = sum(c.elapsed_time(d) for _, _, c, d in evs) / args.steps if world > 1 else 0.0
-    t_k1k4 = sum(a.elapsed_time(b) for a, b in evs_step) / args.steps  # one graph, PDL
-    t_step = t_k1k4 + t_ag
+    t_step = t_k1k4 + (t_ag if world > 1 else 0.0)
     if world > 1:
-        tt = torch.tensor([t_step, t_k1, t_k4, t_ag, t_k1k4], dtype=torch.float64,
-                          device=xt.device)
+        tt = torch.tensor([t_step, t_k1, t_k4, t_ag, t_k1k4], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         t_step, t_k1, t_k4, t_ag, t_k1k4 = tt.tolist()
+    sat_per_step = int(lb.sat.item()) // max(1, lb.k1_runs)
 
     # ---- e2e: the reference-facing drop-in call with HOST f64 buffers ----
-    xh = torch.from_numpy(x).to(torch.bfloat16).double().pin_memory().numpy()
-    yh = torch.empty((m, b1 - b0), dtype=torch.float64).pin_memory().numpy()
-    for _ in range(2):  # warm: the pool grows to the full-size buffers, streams exist
-        fq.check(fq.lib().fqg_layer_run_host(layer._h, xh.ctypes.data, m, yh.ctypes.data,
-                                             ctypes.byref(ctypes.c_int64())))
-    te = []
-    sat = ctypes.c_int64()
-    for _ in range(args.e2e_steps):
-        barrier()
-        t0 = time.perf_counter()
-        fq.check(fq.lib().fqg_layer_run_host(layer._h, xh.ctypes.data, m, yh.ctypes.data,
-                                             ctypes.byref(sat)))
-        te.append(time.perf_counter() - t0)
-    t_e2e = float(np.mean(te))
+    # Plain (pageable) numpy buffers, as fq::gpu::run_layer passes its
+    # std::vector-backed fq::Matrix; the pinned-buffer rate is reported beside it.
+    xh_pageable = np.ascontiguousarray(bf16_round(x))
+    yh_pageable = np.empty((m, b1 - b0))
+    xh_pinned = torch.from_numpy(xh_pageable).pin_memory().numpy()
+    yh_pinned = torch.empty((m, b1 - b0), dtype=torch.float64).pin_memory().numpy()
+
+    def run_host(xh, yh, reps):
+        sat = ctypes.c_int64()
+        ts = []
+        for _ in range(reps):
+            barrier()
+            t0 = time.perf_counter()
+            fq.check(fq.lib().fqg_layer_run_host(layer._h, xh.ctypes.data, m, yh.ctypes.data,
+                                                 ctypes.byref(sat)))
+            ts.append(time.perf_counter() - t0)
+        return float(np.mean(ts))
+
+    run_host(xh_pageable, yh_pageable, 2)  # warm: the pool grows, streams exist
+    run_host(xh_pinned, yh_pinned, 2)
+    t_e2e = run_host(xh_pageable, yh_pageable, args.e2e_steps)
+    t_e2e_pinned = run_host(xh_pinned, yh_pinned, args.e2e_steps)
     if world > 1:
-        tt = torch.tensor([t_e2e], dtype=torch.float64, device=xt.device)
+        tt = torch.tensor([t_e2e, t_e2e_pinned], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_e2e = tt.item()
+        t_e2e, t_e2e_pinned = tt.tolist()
 
     ops = 2.0 * m * n * kp  # whole layer (all ranks), reference bitops K' (pipeline.cpp:211)
     tops = ops / (t_step * 1e-3) / 1e12
     hbm_gbs, bf16_tf, peak_src, int8_peak, i8_src = peaks()
     gemm_ops_rank = 2.0 * m * (b1 - b0) * kp
     gemm_tops = gemm_ops_rank / (t_k4 * 1e-3) / 1e12
+    ldq = kp // 2 if a_fmt == fq.I4 else kp
     k1_bytes = m * k * 2 + m * ldq + kp * 4 + k * 12
     k1_gbs = k1_bytes / (t_k1 * 1e-3) / 1e9
     traffic = None
-    try:
+    try:  # per-launch DRAM bytes of K4 from the committed ncu --set full capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
             tr = json.load(f).get(args.config, {})
             traffic = tr.get("gemm_dram_bytes")
@@ -349,10 +536,12 @@ def main():
                    "flatten_ratio_x": cfg.plan_x.flatten_ratio(),
                    "a_format": "i4 packed" if a_fmt == fq.I4 else "i8",
                    "b_format": "i4 packed" if b_fmt == fq.I4 else "i8",
-                   "out_dtype": "fp16", "parallelism": f"N-shard x{world}" if world > 1 else "1 GPU",
+                   "out_dtype": "fp16",
+                   "parallelism": f"N-shard x{world} + NCCL all-gather" if world > 1 else "1 GPU",
                    "l2": "flushed between timed steps (256 MiB write)"},
-        "breakdown_ms": {"flatten_quant_K1": t_k1, "gemm_K4": t_k4, "all_gather": t_ag,
-                         "K1_K4_graph": t_k1k4},
+        "breakdown_ms": {"flatten_quant_K1": t_k1, "gemm_K4": t_k4,
+                         "all_gather": t_ag if world > 1 else 0.0, "K1_K4_graph": t_k1k4},
+        "saturation_events_per_step": sat_per_step,  # counted by K1 in every timed step
         "roofline": {"bound": "tensor", "achieved": gemm_tops, "peak": int8_peak,
                      "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
                      "kernel": "k_gemm_i8_pair (tcgen05.mma.cta_group::2.kind::i8, 256x512 tiles)",
@@ -365,27 +554,29 @@ def main():
         "e2e": {"value": ops / t_e2e / 1e12, "unit": "TOPS",
                 "tokens_per_s": m / t_e2e,
                 "h2d_bytes_per_step": m * k * 8, "d2h_bytes_per_step": m * (b1 - b0) * 8 + 8,
-                "api": "fqg_layer_run_host (drop-in fq::run_layer, f64 host buffers, pinned)"},
-        "gpu_launches": launches_per_step * args.steps,  # the headline (one-graph) loop;
-        # the per-kernel loop launches the same number again
+                "api": "fqg_layer_run_host (drop-in fq::run_layer), f64 host buffers, pageable "
+                       "(numpy), H2D + kernels + D2H in the timed call",
+                "pinned_host_buffers": {"value": ops / t_e2e_pinned / 1e12, "unit": "TOPS",
+                                        "tokens_per_s": m / t_e2e_pinned}},
+        # per timed step: K1 + K4 (one graph); the per-kernel loop replays them
+        # again from graphs of their own; split-K adds its reduce kernel for small M
+        "gpu_launches": (2 + (1 if m <= 512 else 0)) * args.steps,
         "launch": "one CUDA graph per step (K1, then K4 as a programmatic dependent launch); "
                   "K1 and K4 also timed apart from their own graphs for the rooflines",
         "clocks": clk.summary(),
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        threads = os.cpu_count() or 1
-        rec = __import__("oracle").Layer(
-            bits=bits, s=cfg.smooth_scales, t_x=cfg.plan_x.threshold, e_x=cfg.plan_x.extensions,
-            t_w=cfg.plan_w.threshold, e_w=cfg.plan_w.extensions, wq=layer.weight_q(),
-            s_w=layer.w_scale, act_scale=cfg.act_scale)
-        res = cpu_reference_sample(k, n, bits, rows=args.cpu_rows or m, threads=threads,
-                                   recipe_layer=rec)
-        line["cpu_baseline"] = {
-            "value": res["tops"], "unit": "TOPS", "cores": threads, "kind": "reference",
-            "tokens_per_s": res["tokens_per_s"],
-            "sample": f"{res['rows']} rows of the same layer/recipe, unmodified fq::run_layer "
-                      f"(oracle/_ref) row-parallel on {threads} host threads, "
-                      f"{res['seconds']:.2f} s"}
+    if world > 1:
+        line["collective"] = {"op": "ncclAllGather (torch.distributed all_gather_into_tensor, "
+                                    "in place into the shard-major buffer)",
+                              "bytes_received_per_rank": (world - 1) * m * width * 2,
+                              "ms": t_ag}
+    if rank == 0 and world == 1:
+        del lb
+        torch.cuda.empty_cache()
+        if not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(fq, cfg, layer, bf16_round(x), bits, k, n, m)
+        if not args.no_subresults and args.config == "w4a4_4096":
+            line["subresults"] = subresults(fq, args, int8_peak, flush)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -11,12 +11,16 @@
 // (pipeline.hpp:83-84, pipeline.cpp:159-169): same f64 outputs bit for bit,
 // same saturation count, std::invalid_argument on a channel-count mismatch,
 // std::runtime_error for device failures. The quantized layer is uploaded to
-// HBM on first use and cached per (thread, recipe object, weight buffer);
-// fq::gpu::Layer gives explicit control of that lifetime.
+// HBM on first use and cached process-wide by recipe CONTENT (every field
+// run_layer reads, weights included; LRU, FQG_LAYER_CACHE entries, default 4);
+// fq::gpu::Layer gives explicit control of that lifetime. Host buffers may be
+// pageable: the library stages them through pinned bounce buffers.
 #pragma once
 
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
@@ -89,30 +93,65 @@ class Layer {
     std::int64_t k_ = 0, n_ = 0;
 };
 
-inline const Layer& cached_layer(const LayerQuantConfig& cfg) {
-    struct Entry {
-        const void* weights;
-        std::size_t size;
-        double act_scale;
-        std::unique_ptr<Layer> layer;
+// Content key of a recipe: every field run_layer reads, the weights included
+// (fqg_hash64 is parallel over 1 MiB blocks: ~1 ms per 100 MB of weight_q).
+inline std::uint64_t recipe_key(const LayerQuantConfig& cfg) {
+    std::uint64_t h = 0x6671676b6579ull;  // "fqgkey"
+    auto add = [&h](const void* p, std::size_t n) { h = fqg_hash64(p, n, h); };
+    auto add_plan = [&](const FlattenPlan& p) {
+        add(&p.threshold, sizeof(p.threshold));
+        add(&p.block, sizeof(p.block));
+        add(p.extensions.data(), p.extensions.size() * sizeof(p.extensions[0]));
     };
-    thread_local std::unordered_map<const LayerQuantConfig*, Entry> cache;
-    Entry& e = cache[&cfg];
-    if (!e.layer || e.weights != cfg.weight_q.q.data.data() ||
-        e.size != cfg.weight_q.q.data.size() || e.act_scale != cfg.act_scale) {
-        e.layer = std::make_unique<Layer>(cfg);
-        e.weights = cfg.weight_q.q.data.data();
-        e.size = cfg.weight_q.q.data.size();
-        e.act_scale = cfg.act_scale;
+    add(&cfg.bits, sizeof(cfg.bits));
+    add(&cfg.act_scale, sizeof(cfg.act_scale));
+    add(cfg.smooth_scales.s.data(), cfg.smooth_scales.s.size() * sizeof(double));
+    add_plan(cfg.plan_x);
+    add_plan(cfg.plan_w);
+    add(&cfg.weight_q.params.scale, sizeof(cfg.weight_q.params.scale));
+    add(&cfg.weight_q.q.rows, sizeof(cfg.weight_q.q.rows));
+    add(&cfg.weight_q.q.cols, sizeof(cfg.weight_q.q.cols));
+    add(cfg.weight_q.q.data.data(), cfg.weight_q.q.data.size() * sizeof(cfg.weight_q.q.data[0]));
+    return h;
+}
+
+// Process-wide LRU cache of device layers keyed by recipe content (layers are
+// immutable, so threads share them; capacity FQG_LAYER_CACHE, default 4).
+inline std::shared_ptr<const Layer> cached_layer(const LayerQuantConfig& cfg) {
+    struct Entry {
+        std::uint64_t key;
+        std::shared_ptr<const Layer> layer;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> lru;  // most recently used last
+    static const std::size_t cap = [] {
+        const char* e = std::getenv("FQG_LAYER_CACHE");
+        const long v = e ? std::strtol(e, nullptr, 10) : 4;
+        return static_cast<std::size_t>(v > 0 ? v : 1);
+    }();
+    const std::uint64_t key = recipe_key(cfg);
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        for (std::size_t i = 0; i < lru.size(); ++i)
+            if (lru[i].key == key) {
+                Entry e = lru[i];
+                lru.erase(lru.begin() + static_cast<std::ptrdiff_t>(i));
+                lru.push_back(e);
+                return e.layer;
+            }
     }
-    return *e.layer;
+    auto layer = std::make_shared<const Layer>(cfg);  // outside the lock: uploads weights
+    std::lock_guard<std::mutex> lk(mu);
+    lru.push_back({key, layer});
+    while (lru.size() > cap) lru.erase(lru.begin());
+    return layer;
 }
 
 inline Matrix run_layer(const LayerQuantConfig& cfg, const Matrix& x,
                         std::int64_t& saturation_events) {
     if (x.cols != cfg.plan_x.channels())
         throw std::invalid_argument("run_layer: input channel count does not match recipe");
-    return cached_layer(cfg).run(x, saturation_events);
+    return cached_layer(cfg)->run(x, saturation_events);
 }
 
 inline Matrix run_layer(const LayerQuantConfig& cfg, const Matrix& x) {

@@ -18,6 +18,7 @@
  */
 #ifndef FQG_H
 #define FQG_H
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -118,6 +119,35 @@ int fqg_layer_forward(fqg_layer_t layer, const void* x_dev, int x_dtype, int64_t
                       int y_dtype, int64_t ldy, const void* bias_dev, int bias_dtype,
                       unsigned long long* saturation_dev, void* stream);
 
+/* N-sharding across the GPUs of a node. The layer shards along
+ * N: rank r of `world` holds columns [b0, b1) = fqg_shard_bounds(n_total, world,
+ * r) (create it with desc.n_begin = b0, desc.n = b1 - b0; the device weight tail
+ * uses the GLOBAL s_w, so every shard is an exact column slice). Widths are
+ * 32-aligned except possibly the last; `width` is the common slot width. */
+int fqg_shard_bounds(int64_t n_total, int world, int rank, int64_t* b0, int64_t* b1,
+                     int64_t* width);
+
+/* The collective the caller supplies: ncclAllGather itself fits this type
+ * (sendbuff, recvbuff, sendcount, ncclDataType_t, ncclComm_t, cudaStream_t; the
+ * return value is ncclResult_t, 0 = success), so the library does not link or
+ * load any NCCL and the caller's communicator stays with the NCCL that made it. */
+typedef int (*fqg_allgather_fn)(const void* sendbuff, void* recvbuff, size_t sendcount,
+                                int nccl_datatype, void* comm, void* stream);
+
+/* Sharded fq::run_layer on device data: this rank's K1 + K4 write its column
+ * shard straight into its slot of the shard-major gather buffer
+ * gather_dev [world][m][width] (y_dtype F16/BF16/F32/F64), then `allgather`
+ * fills the other ranks' slots in place (sendbuff = this rank's slot, count
+ * m * width elements). Column c of the full output is slot c / width (for the
+ * 32-aligned widths of fqg_shard_bounds: slot r holds [b0_r, b1_r)), row i at
+ * [r][i][c - b0_r]; no reassembly copy is made. allgather may be NULL (world 1,
+ * or a caller that gathers later). Stream-ordered. */
+int fqg_layer_forward_sharded(fqg_layer_t layer, const void* x_dev, int x_dtype, int64_t m,
+                              void* gather_dev, int y_dtype, int world, int rank,
+                              const void* bias_dev, int bias_dtype,
+                              unsigned long long* saturation_dev, fqg_allgather_fn allgather,
+                              void* comm, void* stream);
+
 /* The drop-in host call: same contract as fq::run_layer(cfg, x, saturation)
  * (pipeline.hpp:84) on host f64 buffers; copies in, runs, copies out,
  * synchronizes. y_host: [m][n] f64, equal to the reference bit for bit. */
@@ -164,6 +194,12 @@ typedef struct fqg_gemm_plan_info {
 } fqg_gemm_plan_info;
 int fqg_gemm_plan(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int y_dtype,
                   fqg_gemm_plan_info* out);
+
+/* 64-bit content hash (host, parallel over fixed 1 MiB blocks; the value does
+ * not depend on the thread count). The C++ shim keys its layer cache on the
+ * hash of every recipe field and the weights, so an edited recipe or a reused
+ * address never returns a stale device layer. */
+uint64_t fqg_hash64(const void* data, size_t bytes, uint64_t seed);
 
 /* Host-side plan arithmetic (pure integer/FP64 work, no device):
  * fq::build_flatten_plan (flatten.cpp:17-45). e/off: [k]. */

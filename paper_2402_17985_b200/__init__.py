@@ -250,6 +250,31 @@ class Layer:
             torch.cuda.current_stream(x.device).cuda_stream))
         return q
 
+    def quantize_acts_rowsum(self, x, saturation=None):
+        """K1 with the operand row sums the biased-int4 GEMM epilogue uses."""
+        import torch
+
+        x = x.contiguous()
+        cols = self.kp // 2 if self.info.a_format == I4 else self.kp
+        q = torch.empty((x.shape[0], cols), dtype=torch.int8, device=x.device)
+        rowsum = torch.empty(x.shape[0], dtype=torch.int32, device=x.device)
+        check(lib().fqg_layer_quantize_acts_ex(
+            self._h, x.data_ptr(), _torch_dtype_code(x), x.shape[0], q.data_ptr(),
+            rowsum.data_ptr(), saturation.data_ptr() if saturation is not None else None,
+            torch.cuda.current_stream(x.device).cuda_stream))
+        return q, rowsum
+
+    def gemm_rows(self, q, rowsum, r0: int, rows: int, out, bias=None):
+        """K4 on operand rows [r0, r0 + rows) into `out` ([rows, n] view, any row stride)."""
+        import torch
+
+        check(lib().fqg_layer_gemm_ex(
+            self._h, q[r0:].data_ptr(), rowsum[r0:].data_ptr(), rows, out.data_ptr(),
+            _torch_dtype_code(out), out.stride(0), bias.data_ptr() if bias is not None else None,
+            _torch_dtype_code(bias) if bias is not None else NONE,
+            torch.cuda.current_stream(q.device).cuda_stream))
+        return out
+
     def gemm(self, q, out_dtype=None, bias=None, out=None):
         """K4 alone on an operand from :meth:`quantize_acts`."""
         import torch

@@ -93,6 +93,11 @@ class SynthOpts(C.Structure):
     ]
 
 
+# ncclAllGather-compatible collective (include/fqg.h fqg_allgather_fn)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p,
+                           C.c_void_p)
+
+
 class GemmPlan(C.Structure):
     _fields_ = [("kernel", INT), ("tile_m", INT), ("tile_n", INT), ("splits", INT), ("ctas", INT)]
 
@@ -113,6 +118,9 @@ SIGNATURES = {
     "fqg_layer_gemm_ex": (INT, [P, P, P, I64, P, INT, I64, P, INT, P]),
     "fqg_gemm": (INT, [P, INT, I64, P, INT, I64, I64, I64, I64, P, INT, I64, P, P, INT, P]),
     "fqg_gemm_plan": (INT, [I64, I64, I64, INT, INT, INT, C.POINTER(GemmPlan)]),
+    "fqg_shard_bounds": (INT, [I64, INT, INT, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
+    "fqg_layer_forward_sharded": (INT, [P, P, INT, I64, P, INT, INT, INT, P, INT, P, P, P, P]),
+    "fqg_hash64": (C.c_uint64, [P, C.c_size_t, C.c_uint64]),
     "fqg_build_flatten_plan": (INT, [P, I64, F64_, I64, P, P, C.POINTER(I64), C.POINTER(I64)]),
     "fqg_split_against_threshold": (None, [F64_, F64_, C.POINTER(I64), C.POINTER(F64_)]),
     "fqg_recipe_plan": (INT, [P, I64, I64, P, INT, F64_, F64_, I64, INT, INT, P,

@@ -81,7 +81,9 @@ GemmPlan plan_gemm(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int v
     // Measured at 2048 x 4096 x 7488: pair 61 us (int8 weights) / 71 us (biased
     // int4), single-CTA 71 us (int4); a weights-in-TMEM variant (unpacked int4
     // weights as the MMA's A operand in TMEM) measured 79-87 us and was removed.
-    if (v == 0) v = (m > BM && n > 128 && a_fmt == FQG_I8) ? 2 : 1;
+    // The pair kernel also for small M: its split-K spreads the weight stream over
+    // the CTA pairs (M = 1 at 8192^2: 61 us on 32 single CTAs before).
+    if (v == 0) v = (n > 128 && a_fmt == FQG_I8) ? 2 : 1;
     const int64_t num_kb = (kp + BK - 1) / BK;
     if (v == 2) {
         p.kernel = 2;

@@ -10,13 +10,19 @@
 //   d_scale f64 [2]       {s_x, s_w}
 // Per forward (stream-ordered allocations): q [M][ldq] int8 / packed int4.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <vector>
 
 #include "fqg_internal.h"
 #include "host.h"
+#include "host_pool.h"
 #include "kernels.h"
 
 namespace fqg {
@@ -378,6 +384,31 @@ void forward(const fqg_layer_s* L, const void* x, int x_dtype, int64_t m, void* 
     run_gemm(L, cs.q, rowsum, m, y, y_dtype, ldy, scale, bias, bias_dtype, st);
 }
 
+// Pinned bounce buffers per (thread, device), grown on demand.
+struct Bounce {
+    void* p = nullptr;
+    size_t cap = 0;
+    void* get(size_t bytes) {
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            cap = 0;
+            FQG_CUDA(cudaHostAlloc(&p, bytes, cudaHostAllocDefault));
+            cap = bytes;
+        }
+        return p;
+    }
+};
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
 }  // namespace
 }  // namespace fqg
 
@@ -478,6 +509,50 @@ int fqg_layer_gemm(fqg_layer_t L, const void* q, int64_t m, void* y, int y_dtype
     return fqg_layer_gemm_ex(L, q, nullptr, m, y, y_dtype, ldy, bias, bias_dtype, stream);
 }
 
+int fqg_shard_bounds(int64_t n_total, int world, int rank, int64_t* b0, int64_t* b1,
+                     int64_t* width) {
+    return guard([&] {
+        require(n_total >= 1 && world >= 1 && rank >= 0 && rank < world,
+                "shard_bounds: bad rank/world");
+        int64_t per = (n_total + world - 1) / world;
+        per = (per + 31) / 32 * 32;  // 32-aligned shards (the GEMM's K-major int4 groups)
+        const int64_t s0 = std::min<int64_t>(n_total, static_cast<int64_t>(rank) * per);
+        if (b0) *b0 = s0;
+        if (b1) *b1 = std::min<int64_t>(n_total, s0 + per);
+        if (width) *width = std::min<int64_t>(n_total, per);
+    });
+}
+
+int fqg_layer_forward_sharded(fqg_layer_t L, const void* x, int x_dtype, int64_t m, void* gather,
+                              int y_dtype, int world, int rank, const void* bias, int bias_dtype,
+                              unsigned long long* saturation_dev, fqg_allgather_fn allgather,
+                              void* comm, void* stream) {
+    return guard([&] {
+        require(L != nullptr && x && gather && m >= 1, "forward_sharded: bad argument");
+        require(world >= 1 && rank >= 0 && rank < world, "forward_sharded: bad rank/world");
+        require(y_dtype == FQG_F16 || y_dtype == FQG_BF16 || y_dtype == FQG_F32 ||
+                    y_dtype == FQG_F64,
+                "forward_sharded: output dtype must be F16/BF16/F32/F64");
+        int64_t b0 = 0, b1 = 0, width = 0;
+        if (fqg_shard_bounds(L->n_total, world, rank, &b0, &b1, &width) != FQG_OK)
+            throw Error(FQG_ERR_INVALID, g_last_error);
+        require(b0 == L->n_begin && b1 - b0 == L->n,
+                "forward_sharded: the layer is not this rank's fqg_shard_bounds shard");
+        DeviceGuard dg(L->device);
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        const int esz = dtype_size(y_dtype);
+        uint8_t* slot = static_cast<uint8_t*>(gather) + static_cast<size_t>(rank) * m * width * esz;
+        forward(L, x, x_dtype, m, slot, y_dtype, width, bias, bias_dtype, saturation_dev, st);
+        if (allgather != nullptr && world > 1) {
+            // ncclDataType_t: ncclFloat16 = 6, ncclFloat32 = 7, ncclFloat64 = 8, ncclBfloat16 = 9
+            const int nt = y_dtype == FQG_F16 ? 6 : y_dtype == FQG_F32 ? 7 : y_dtype == FQG_F64 ? 8 : 9;
+            const int rc = allgather(slot, gather, static_cast<size_t>(m * width), nt, comm, stream);
+            if (rc != 0)
+                throw Error(FQG_ERR_RUNTIME, "forward_sharded: allgather returned " + std::to_string(rc));
+        }
+    });
+}
+
 // The drop-in host call, pipelined: M is cut into row chunks that alternate
 // between two streams, so the host->device copy of chunk c + 1, the kernels of
 // chunk c and the device->host copy of chunk c - 1 overlap (PCIe is full
@@ -526,18 +601,63 @@ int fqg_layer_run_host(fqg_layer_t L, const double* x_host, int64_t m, double* y
         const int64_t chunk = L->scale_mode == FQG_SCALE_DYNAMIC
                                   ? m
                                   : std::max<int64_t>(128, ((m + 7) / 8 + 31) / 32 * 32);
+        // Pageable host buffers (the drop-in's fq::Matrix) are staged through
+        // pinned bounce buffers, two chunk slots each way: the parallel host copy
+        // of chunk c overlaps the DMA and kernels of chunks c - 1 and c - 2.
+        const bool staged = !(is_pinned(x_host) && is_pinned(y_host));
+        static thread_local Bounce bx[64][2], by[64][2];
+        static thread_local cudaEvent_t evx[64][2] = {}, evy[64][2] = {};
+        cudaEvent_t* ex = evx[L->device & 63];
+        cudaEvent_t* ey = evy[L->device & 63];
+        for (int i = 0; i < 2 && staged; ++i) {
+            if (ex[i] == nullptr) FQG_CUDA(cudaEventCreateWithFlags(&ex[i], cudaEventDisableTiming));
+            if (ey[i] == nullptr) FQG_CUDA(cudaEventCreateWithFlags(&ey[i], cudaEventDisableTiming));
+        }
+        const size_t cxb = static_cast<size_t>(chunk * L->k) * 8, cyb = static_cast<size_t>(chunk * L->n) * 8;
+        struct Pending {
+            int64_t r0 = 0, mc = 0;
+            bool live = false;
+        } pend[2];
+        auto drain = [&](int slot) {  // chunk in y slot `slot` -> the caller's buffer
+            if (!pend[slot].live) return;
+            FQG_CUDA(cudaEventSynchronize(ey[slot]));
+            parallel_copy(y_host + pend[slot].r0 * L->n, by[L->device & 63][slot].p,
+                                 static_cast<size_t>(pend[slot].mc * L->n) * 8);
+            pend[slot].live = false;
+        };
         int ci = 0;
         for (int64_t r0 = 0; r0 < m; r0 += chunk, ++ci) {
             const int64_t mc = std::min(chunk, m - r0);
-            cudaStream_t s = ss[ci & 1];
+            const int slot = ci & 1;
+            cudaStream_t s = ss[slot];
             const double* xs = x_host + r0 * L->k;
             double* dxs = static_cast<double*>(dx) + r0 * L->k;
             double* dys = static_cast<double*>(dy) + r0 * L->n;
-            FQG_CUDA(cudaMemcpyAsync(dxs, xs, static_cast<size_t>(mc * L->k) * 8,
-                                     cudaMemcpyHostToDevice, s));
+            const size_t nxb = static_cast<size_t>(mc * L->k) * 8, nyb = static_cast<size_t>(mc * L->n) * 8;
+            if (staged) {
+                void* px = bx[L->device & 63][slot].get(cxb);
+                by[L->device & 63][slot].get(cyb);
+                if (ci >= 2) FQG_CUDA(cudaEventSynchronize(ex[slot]));  // H2D of chunk c-2 read it
+                parallel_copy(px, xs, nxb);
+                FQG_CUDA(cudaMemcpyAsync(dxs, px, nxb, cudaMemcpyHostToDevice, s));
+                FQG_CUDA(cudaEventRecord(ex[slot], s));
+            } else {
+                FQG_CUDA(cudaMemcpyAsync(dxs, xs, nxb, cudaMemcpyHostToDevice, s));
+            }
             forward(L, dxs, FQG_F64, mc, dys, FQG_F64, L->n, nullptr, FQG_NONE, dsat, s);
-            FQG_CUDA(cudaMemcpyAsync(y_host + r0 * L->n, dys, static_cast<size_t>(mc * L->n) * 8,
-                                     cudaMemcpyDeviceToHost, s));
+            if (staged) {
+                drain(slot);  // chunk c - 2 leaves the y slot before chunk c's D2H lands
+                FQG_CUDA(cudaMemcpyAsync(by[L->device & 63][slot].p, dys, nyb,
+                                         cudaMemcpyDeviceToHost, s));
+                FQG_CUDA(cudaEventRecord(ey[slot], s));
+                pend[slot] = {r0, mc, true};
+            } else {
+                FQG_CUDA(cudaMemcpyAsync(y_host + r0 * L->n, dys, nyb, cudaMemcpyDeviceToHost, s));
+            }
+        }
+        if (staged) {
+            drain(ci & 1);  // the older of the two outstanding chunks first
+            drain((ci + 1) & 1);
         }
         FQG_CUDA(cudaEventRecord(ev[1], ss[1]));
         FQG_CUDA(cudaStreamWaitEvent(st, ev[1], 0));

@@ -34,11 +34,10 @@ def shard_width(n: int, world: int, align: int = 32) -> int:
 
 
 def gather_columns(y_local, n: int, group=None, align: int = 32):
-    """All-gather [M, n_r] column shards into the full [M, n] output.
-
-    all_gather_into_tensor needs equal contributions, so each rank pads its
-    shard to the common width; the result is reassembled column-block by
-    column-block (the collective returns [world, M, width])."""
+    """All-gather [M, n_r] column shards into the full [M, n] output (host-logic
+    helper for tests and small tensors: pads and reassembles with copies; the
+    device path, ShardedLayer.forward, writes each shard straight into its slot
+    of a shard-major buffer and gathers in place instead)."""
     import torch
     import torch.distributed as dist
 
@@ -49,38 +48,92 @@ def gather_columns(y_local, n: int, group=None, align: int = 32):
     b0, b1 = shard_bounds(n, world, rank, align)
     if y_local.shape[1] != b1 - b0:
         raise ValueError("gather_columns: local shard width mismatch")
-    send = y_local
-    if y_local.shape[1] != width:
-        send = torch.zeros((m, width), dtype=y_local.dtype, device=y_local.device)
-        send[:, : b1 - b0] = y_local
-    flat = torch.empty((world * m, width), dtype=y_local.dtype, device=y_local.device)
-    dist.all_gather_into_tensor(flat, send.contiguous(), group=group)
-    out = flat.view(world, m, width)
-    parts = []
-    for r in range(world):
-        c0, c1 = shard_bounds(n, world, r, align)
-        if c1 > c0:
-            parts.append(out[r, :, : c1 - c0])
-    return torch.cat(parts, dim=1)
+    buf = torch.empty((world, m, width), dtype=y_local.dtype, device=y_local.device)
+    buf[rank, :, : b1 - b0] = y_local
+    dist.all_gather_into_tensor(buf.view(world * m, width), buf[rank], group=group)
+    return ShardedOutput(buf.unsqueeze(0), n, world, align).full()
+
+
+class ShardedOutput:
+    """The gathered layer output in shard-major layout [chunks][world][Mc][width]
+    (slot r holds columns [b0_r, b1_r) of fqg_shard_bounds). No reassembly copy
+    is made unless full() is called."""
+
+    def __init__(self, buf, n: int, world: int, align: int = 32):
+        self.buf, self.n, self.world, self.align = buf, n, world, align
+
+    def shard(self, r: int):
+        """Rank r's columns as an [M, b1 - b0] view (rows of all chunks)."""
+        b0, b1 = shard_bounds(self.n, self.world, r, self.align)
+        c, w, mc, width = self.buf.shape
+        return self.buf[:, r, :, : b1 - b0].reshape(c * mc, b1 - b0)
+
+    def full(self):
+        """[M, N] contiguous copy (one permute-copy of the gathered slots). Slots
+        are in column order and only the last non-empty one can be narrower, so
+        the padding columns all land at the end."""
+        c, w, mc, width = self.buf.shape
+        return self.buf.permute(0, 2, 1, 3).reshape(c * mc, w * width)[:, : self.n]
 
 
 class ShardedLayer:
-    """One rank's column shard of a layer (device weights of columns [b0, b1))."""
+    """One rank's column shard of a layer (device weights of columns [b0, b1)).
 
-    def __init__(self, cfg, rank: int, world: int, device: Optional[int] = None, **layer_kw):
-        from . import Layer
+    forward() runs K1 on the replicated input, then K4 per M-chunk straight into
+    this rank's slot of the shard-major buffer [chunks][world][Mc][width], and
+    all-gathers each chunk in place on a communication stream, so the gather of
+    chunk c overlaps the GEMM of chunk c + 1 (NCCL over NVLink on the GPU path)."""
 
+    def __init__(self, cfg, rank: int, world: int, device: Optional[int] = None, layer=None,
+                 **layer_kw):
         self.n = cfg.n
         self.rank, self.world = rank, world
         self.b0, self.b1 = shard_bounds(self.n, world, rank)
+        self.width = shard_width(self.n, world)
         if self.b1 <= self.b0:
             raise ValueError("ShardedLayer: this rank holds no columns")
-        self.layer = Layer(cfg, device=rank if device is None else device, n_begin=self.b0,
-                           n=self.b1 - self.b0, **layer_kw)
+        if layer is None:  # `layer`: an injected stand-in (CPU tests of the host logic)
+            from . import Layer
 
-    def forward(self, x, gather: bool = True, **kw):
-        y = self.layer.forward(x, **kw)
-        return gather_columns(y, self.n) if gather else y
+            layer = Layer(cfg, device=rank if device is None else device, n_begin=self.b0,
+                          n=self.b1 - self.b0, **layer_kw)
+        self.layer = layer
+        self._comm = None
+
+    def forward(self, x, out_dtype=None, gather: bool = True, chunks: int = 1, group=None):
+        import torch
+        import torch.distributed as dist
+
+        m = x.shape[0]
+        if chunks < 1 or m % chunks != 0:
+            chunks = 1
+        mc = m // chunks
+        dt = out_dtype or torch.float16
+        buf = torch.empty((chunks, self.world, mc, self.width), dtype=dt, device=x.device)
+        L = self.layer
+        on_gpu = x.is_cuda
+        st = torch.cuda.current_stream(x.device) if on_gpu else None
+        q, rowsum = L.quantize_acts_rowsum(x)
+        if on_gpu and gather and self.world > 1 and self._comm is None:
+            self._comm = torch.cuda.Stream(x.device)
+        for c in range(chunks):
+            out = buf[c, self.rank, :, : self.b1 - self.b0]
+            L.gemm_rows(q, rowsum, c * mc, mc, out)
+            if not (gather and self.world > 1):
+                continue
+            dst, src = buf[c].view(self.world * mc, self.width), buf[c, self.rank]
+            if on_gpu:  # gather of chunk c overlaps the GEMM of chunk c + 1
+                ev = torch.cuda.Event()
+                ev.record(st)
+                self._comm.wait_event(ev)
+                with torch.cuda.stream(self._comm):
+                    dist.all_gather_into_tensor(dst, src, group=group)
+            else:
+                dist.all_gather_into_tensor(dst, src, group=group)
+        if on_gpu and gather and self.world > 1:
+            st.wait_stream(self._comm)
+            buf.record_stream(self._comm)
+        return ShardedOutput(buf, self.n, self.world)
 
 
 def emulate_shard_outputs(acc_full: np.ndarray, s_x: float, s_w: float, world: int):

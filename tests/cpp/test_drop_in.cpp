@@ -74,6 +74,21 @@ int main() {
                   s1 == s2,
               "fq::gpu::Layer explicit handle");
     }
+    {  // the layer cache is keyed by recipe content: an in-place edit at the same
+       // address (e.g. O2 weights replaced by O3 GPTQ weights) is never served stale
+        const fq::SyntheticLayer L = fq::make_synthetic_layer(so, 1);
+        fq::LayerQuantConfig cfg = fq::quantize_layer(L.weight, L.calib, fq::QuantOptions{});
+        const fq::Matrix y0 = fq::gpu::run_layer(cfg, L.test_input);
+        const auto* addr = cfg.weight_q.q.data.data();
+        for (auto& v : cfg.weight_q.q.data) v = -v;
+        const fq::Matrix y1 = fq::gpu::run_layer(cfg, L.test_input);
+        check(addr == cfg.weight_q.q.data.data() && y1 == fq::run_layer(cfg, L.test_input) &&
+                  !(y1 == y0),
+              "in-place weight edit at the same address is not served from the cache");
+        cfg.act_scale *= 0.5;
+        check(fq::gpu::run_layer(cfg, L.test_input) == fq::run_layer(cfg, L.test_input),
+              "edited act_scale is not served from the cache");
+    }
     std::printf("%s (%d failures)\n", failures ? "FAILED" : "ALL PASS", failures);
     return failures ? 1 : 0;
 }

@@ -72,3 +72,51 @@ def test_dynamic_scale_run_host_is_one_tensor_absmax(port, fq):
     layer = fq.Layer(_cfg(fq, L), scale_mode=fq.SCALE_DYNAMIC)
     y, _ = layer.run_layer(x)
     assert np.array_equal(y, y_ref)
+
+
+def test_forward_sharded_c_abi_emulated_two_ranks(port, fq):
+    """fqg_layer_forward_sharded: each rank's shard lands in its slot of the
+    shard-major buffer and the caller's ncclAllGather-shaped collective is called
+    with (this slot, the buffer, m * width, ncclFloat16). Two ranks emulated on
+    one GPU share the buffer, so the collective is a recorded no-op."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2402_17985_b200 import _lib
+
+    k, n, m, world = 1024, 1000, 384, 2
+    w, calib, x = fq.synthetic_layer(4, test_rows=m, in_channels=k, out_channels=n, rows=32,
+                                     samples=4)
+    cfg = fq.quantize_layer(w, calib, 4)
+    xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    full = fq.Layer(cfg, b_format=fq.I4).forward(xt, out_dtype=torch.float16)
+    width = C.c_int64()
+    fq.check(fq.lib().fqg_shard_bounds(n, world, 0, None, None, C.byref(width)))
+    buf = torch.empty((world, m, width.value), dtype=torch.float16, device="cuda")
+    calls = []
+
+    @_lib.ALLGATHER_FN
+    def fake_allgather(send, recv, count, dtype, comm, stream):
+        calls.append((send, recv, count, dtype, comm))
+        return 0
+
+    st = torch.cuda.current_stream().cuda_stream
+    for rank in range(world):
+        b0, b1 = C.c_int64(), C.c_int64()
+        fq.check(fq.lib().fqg_shard_bounds(n, world, rank, C.byref(b0), C.byref(b1), None))
+        layer = fq.Layer(cfg, b_format=fq.I4, n_begin=b0.value, n=b1.value - b0.value)
+        fq.check(fq.lib().fqg_layer_forward_sharded(
+            layer._h, xt.data_ptr(), fq.BF16, m, buf.data_ptr(), fq.F16, world, rank, None,
+            fq.NONE, None, fake_allgather, C.c_void_p(1234), st))
+        torch.cuda.synchronize()
+        slot = buf.data_ptr() + rank * m * width.value * 2
+        assert calls[-1] == (slot, buf.data_ptr(), m * width.value, 6, 1234)
+    y = buf.permute(1, 0, 2).reshape(m, world * width.value)[:, :n]
+    assert torch.equal(y, full)
+    # a layer that is not the rank's shard is refused
+    wrong = fq.Layer(cfg, b_format=fq.I4, n_begin=0, n=256)
+    with pytest.raises(fq.FqgError):
+        fq.check(fq.lib().fqg_layer_forward_sharded(
+            wrong._h, xt.data_ptr(), fq.BF16, m, buf.data_ptr(), fq.F16, world, 0, None, fq.NONE,
+            None, None, None, st))

@@ -18,7 +18,8 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 PATHS = {  # name: (M, N, K', expected plan {kernel, tile_n, splits>1})
-    "one_cta": (100, 640, 512, (1, None, False)),
+    "one_cta": (100, 128, 512, (1, None, False)),
+    "pair_small_m_splitk": (100, 2048, 2048, (2, 256, True)),
     "pair_256x256": (1024, 2560, 512, (2, 256, False)),
     "pair_256x512": (2048, 3072, 256, (2, 512, False)),
     "splitk_reduce": (256, 1024, 2048, (2, 256, True)),
