@@ -195,6 +195,57 @@ typedef struct fqg_gemm_plan_info {
 int fqg_gemm_plan(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int y_dtype,
                   fqg_gemm_plan_info* out);
 
+/* fq::quantize_layer (pipeline.cpp:76-152) for modes O1/O2 with its scans on
+ * the device: calibration channel maxima (collect_channel_maxes,
+ * calibration.cpp:9-28), weight row maxima, and the KL bit-width selection
+ * (select_bit_width, quantize.cpp:145-158: P / INT4 / INT8 round-trip
+ * histograms of the flattened calibration activations and of the flattened
+ * weight). Smoothing scales, boxplot truncation and the plans are host
+ * arithmetic on K values. The recipe (bits, s, plans, T_x, T_w, act_scale, s_w,
+ * KL ratios) equals the reference's bit for bit; the layer is then created with
+ * desc.weight = W (the device weight tail computes the same weight_q).
+ * weight: host f64 [k][n]; calib: host f64 [samples][rows][k]. */
+typedef struct fqg_quant_options {
+    int mode;            /* 1 = O1 (8 bits pinned), 2 = O2 (KL choice) */
+    double alpha, beta, gamma;
+    int64_t block, bins;
+    int smooth, clip;
+} fqg_quant_options;
+void fqg_quant_options_default(fqg_quant_options* o);  /* pipeline.hpp:24-34 */
+typedef struct fqg_recipe_s* fqg_recipe_t;
+int fqg_calibrate(const double* weight, int64_t k, int64_t n, const double* calib, int64_t samples,
+                  int64_t rows, const fqg_quant_options* options, int device, fqg_recipe_t* out);
+/* The recipe as a layer description (arrays owned by the recipe; weight and
+ * weight_q are NULL: set desc.weight = W before fqg_layer_create). */
+int fqg_recipe_get(fqg_recipe_t recipe, fqg_layer_desc* desc, double* kl_ratio_act,
+                   double* kl_ratio_w);
+int fqg_recipe_free(fqg_recipe_t recipe);
+
+/* The reference's on-disk contract (recipe JSON + FQTA archive) -> device
+ * layers: replaces the CLI's load_recipes (flattenquant_cli.cpp:241-252, over
+ * schemas.cpp:268-298 parse_recipe_json and archive.cpp:144-192
+ * decode_archive). One layer per recipe entry, weights from
+ * "<layer>.qweight" (int32 [K'][N]); 4-bit layers keep int4 weights packed in
+ * HBM and take activations as `a_format` (FQG_I8 or FQG_I4). device < 0 parses
+ * only (no layers; qmodel_path may be NULL). Errors carry the reference's texts
+ * ("missing tensor: ...", "plan: inconsistent extension counts", ...). */
+typedef struct fqg_model_s* fqg_model_t;
+int fqg_model_load(const char* recipe_path, const char* qmodel_path, int device, int a_format,
+                   fqg_model_t* out);
+int fqg_model_destroy(fqg_model_t model);
+int fqg_model_num_layers(fqg_model_t model, int64_t* n);
+int fqg_model_layer_name(fqg_model_t model, int64_t index, char* buf, int64_t cap);
+/* The parsed recipe of layer `index` (arrays owned by the model). */
+int fqg_model_layer_recipe(fqg_model_t model, int64_t index, fqg_layer_desc* desc,
+                           double* kl_ratio_act, double* kl_ratio_w);
+/* The device layer of a recipe entry (owned by the model). */
+int fqg_model_layer(fqg_model_t model, const char* name, fqg_layer_t* layer);
+/* cmd_infer (flattenquant_cli.cpp:254-281): every f64 "<layer>/<name>" tensor of
+ * the input FQTA archive through its layer; outputs (same names, f64 [rows][N],
+ * equal to the reference bit for bit) written as an FQTA archive. */
+int fqg_model_infer(fqg_model_t model, const char* input_path, const char* out_path,
+                    int64_t* saturated_total, int64_t* ran);
+
 /* 64-bit content hash (host, parallel over fixed 1 MiB blocks; the value does
  * not depend on the thread count). The C++ shim keys its layer cache on the
  * hash of every recipe field and the weights, so an edited recipe or a reused

@@ -332,6 +332,10 @@ class Ref:
         L.fqref_layer_from_arrays.argtypes = [C.c_int, I64, I64, _f64p, F64, _i64p, I64, F64,
                                               _i64p, I64, _i32p, F64, F64, C.POINTER(P)]
         L.fqref_layer_free.argtypes = [P]
+        L.fqref_write_model.argtypes = [P, P, I64, C.c_char_p, C.c_char_p]
+        L.fqref_write_f64_archive.argtypes = [C.c_char_p, P, P, P, P, I64]
+        L.fqref_infer.argtypes = [C.c_char_p, C.c_char_p, C.c_char_p, C.c_char_p,
+                                  C.POINTER(I64), C.POINTER(I64)]
         L.fqref_layer_info_get.argtypes = [P, C.POINTER(Ref.Info)]
         L.fqref_layer_arrays.argtypes = [P, P, P, P, P]
         L.fqref_run_layer.argtypes = [P, _f64p, I64, _f64p, C.POINTER(I64), C.c_int]
@@ -377,6 +381,32 @@ class Ref:
         return w, calib, x, idx[: cnt.value].copy()
 
     # -- pipeline.cpp ----------------------------------------------------
+    def write_model(self, layers, names, recipe_path: str, qmodel_path: str) -> None:
+        """cmd_quantize's outputs (flattenquant_cli.cpp:199-238): recipe JSON via the
+        reference's schemas.cpp, "<layer>.qweight" FQTA archive via archive.cpp."""
+        hs = (P * len(layers))(*[l.h for l in layers])
+        ns = (C.c_char_p * len(names))(*[n.encode() for n in names])
+        self._c(self.lib.fqref_write_model(hs, ns, len(layers), recipe_path.encode(),
+                                           qmodel_path.encode()), "write_model")
+
+    def write_f64_archive(self, path: str, tensors: dict) -> None:
+        items = [(k, np.ascontiguousarray(v, np.float64)) for k, v in tensors.items()]
+        n = len(items)
+        names = (C.c_char_p * n)(*[k.encode() for k, _ in items])
+        data = (P * n)(*[v.ctypes.data for _, v in items])
+        rows = (I64 * n)(*[v.shape[0] for _, v in items])
+        cols = (I64 * n)(*[v.shape[1] for _, v in items])
+        self._c(self.lib.fqref_write_f64_archive(path.encode(), names, data, rows, cols, n),
+                "write_f64_archive")
+
+    def infer(self, qmodel_path: str, recipe_path: str, input_path: str, out_path: str):
+        """The reference cmd_infer: -> (saturated elements, tensors run)."""
+        sat, ran = I64(), I64()
+        self._c(self.lib.fqref_infer(qmodel_path.encode(), recipe_path.encode(),
+                                     input_path.encode(), out_path.encode(), C.byref(sat),
+                                     C.byref(ran)), "infer")
+        return sat.value, ran.value
+
     def quantize_layer(self, w, calib, mode: int = 1, **kw) -> "RefLayer":
         w = np.ascontiguousarray(w, np.float64)
         calib = np.ascontiguousarray(calib, np.float64)

@@ -15,11 +15,13 @@
 #include <thread>
 #include <vector>
 
+#include "fq/archive.hpp"
 #include "fq/calibration.hpp"
 #include "fq/flatten.hpp"
 #include "fq/matrix.hpp"
 #include "fq/pipeline.hpp"
 #include "fq/quantize.hpp"
+#include "fq/schemas.hpp"
 #include "fq/smoothing.hpp"
 #include "fq/synthetic.hpp"
 
@@ -386,6 +388,72 @@ int fqref_smoothing_scales(const double* act_max, const double* w_max, int64_t k
                                                            std::span<const double>(w_max, k),
                                                            alpha);
         std::copy(r.s.begin(), r.s.end(), s);
+    });
+}
+
+// The on-disk contract of the reference CLI (flattenquant_cli.cpp:199-238
+// cmd_quantize, :241-281 load_recipes / cmd_infer), driven through the
+// reference's own schemas.cpp (recipe JSON) and archive.cpp (FQTA): `layers`
+// recipes named names[i] are written as recipe.json + <qmodel> with
+// "<layer>.qweight" int32 tensors, exactly as cmd_quantize writes them.
+int fqref_write_model(const fqref_layer* const* layers, const char* const* names, int64_t count,
+                      const char* recipe_path, const char* qmodel_path) {
+    return guard([&] {
+        fq::TensorArchive qmodel;
+        fq::RecipeFile recipe;
+        recipe.options = layers[0]->cfg.options;
+        for (int64_t i = 0; i < count; ++i) {
+            qmodel.add(std::string(names[i]) + ".qweight", layers[i]->cfg.weight_q.q);
+            recipe.layers.push_back({names[i], layers[i]->cfg});
+        }
+        fq::write_archive(qmodel, qmodel_path);
+        fq::save_text(recipe_path, fq::to_json(recipe));
+    });
+}
+
+// An FQTA archive of f64 tensors (names[i], rows[i] x cols[i], data[i]).
+int fqref_write_f64_archive(const char* path, const char* const* names, const double* const* data,
+                            const int64_t* rows, const int64_t* cols, int64_t count) {
+    return guard([&] {
+        fq::TensorArchive a;
+        for (int64_t i = 0; i < count; ++i) a.add(names[i], mat(data[i], rows[i], cols[i]));
+        fq::write_archive(a, path);
+    });
+}
+
+// cmd_infer (flattenquant_cli.cpp:254-281) with load_recipes (:241-252): the
+// reference's own parse_recipe_json + read_archive + run_layer + write_archive.
+int fqref_infer(const char* qmodel_path, const char* recipe_path, const char* input_path,
+                const char* out_path, int64_t* saturated_total, int64_t* ran_out) {
+    return guard([&] {
+        const fq::RecipeFile recipe = fq::parse_recipe_json(fq::load_text(recipe_path));
+        const fq::TensorArchive qmodel = fq::read_archive(qmodel_path);
+        std::vector<std::pair<std::string, fq::LayerQuantConfig>> configs;
+        for (const auto& rec : recipe.layers) {
+            fq::LayerQuantConfig cfg = rec.config;
+            cfg.weight_q.q = qmodel.require(rec.layer + ".qweight").int_matrix();
+            configs.emplace_back(rec.layer, std::move(cfg));
+        }
+        const fq::TensorArchive inputs = fq::read_archive(input_path);
+        fq::TensorArchive outputs;
+        std::int64_t sat_total = 0, ran = 0;
+        for (const auto& entry : inputs.entries) {
+            const auto slash = entry.name.find('/');
+            if (slash == std::string::npos || !entry.is_float()) continue;
+            const std::string layer = entry.name.substr(0, slash);
+            const fq::LayerQuantConfig* cfg = nullptr;
+            for (const auto& c : configs)
+                if (c.first == layer) cfg = &c.second;
+            if (cfg == nullptr) throw std::runtime_error("no recipe for " + layer);
+            std::int64_t sat = 0;
+            outputs.add(entry.name, fq::run_layer(*cfg, entry.matrix(), sat));
+            sat_total += sat;
+            ++ran;
+        }
+        if (ran == 0) throw std::runtime_error("input archive has no <layer>/<name> tensors");
+        fq::write_archive(outputs, out_path);
+        if (saturated_total) *saturated_total = sat_total;
+        if (ran_out) *ran_out = ran;
     });
 }
 

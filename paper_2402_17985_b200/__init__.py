@@ -34,7 +34,7 @@ from ._lib import (BF16, F16, F32, F64, I4, I8, I32, NONE, SCALE_DYNAMIC, SCALE_
 
 __all__ = [
     "FlattenPlan", "build_flatten_plan", "split_against_threshold", "LayerQuantConfig",
-    "Layer", "quantize_layer", "run_layer", "synthetic_layer", "FqgError",
+    "Layer", "Model", "calibrate", "quantize_layer", "run_layer", "synthetic_layer", "FqgError",
     "FqgInvalidArgument", "FqgRuntimeError",
 ]
 
@@ -288,6 +288,98 @@ class Layer:
             _torch_dtype_code(bias) if bias is not None else NONE,
             torch.cuda.current_stream(q.device).cuda_stream))
         return out
+
+
+def calibrate(weight, calib, mode: int = 2, device: int = 0, **opts):
+    """fq::quantize_layer (pipeline.cpp:76-152, modes O1 = 1 / O2 = 2) with the
+    calibration scans and the KL bit selection on the device. weight f64 [K, N],
+    calib f64 [samples, rows, K]. Returns (LayerQuantConfig with weight = W, info)
+    where info holds the KL ratios and the recipe's s_w."""
+    o = _lib.QuantOptions()
+    lib().fqg_quant_options_default(C.byref(o))
+    o.mode = mode
+    for key, v in opts.items():
+        setattr(o, key, v)
+    w = _f64(weight)
+    c = _f64(calib)
+    if c.ndim == 2:
+        c = c[None]
+    h = C.c_void_p()
+    check(lib().fqg_calibrate(w.ctypes.data, w.shape[0], w.shape[1], c.ctypes.data, c.shape[0],
+                              c.shape[1], C.byref(o), device, C.byref(h)))
+    try:
+        d = _lib.LayerDesc()
+        ka, kw = C.c_double(), C.c_double()
+        check(lib().fqg_recipe_get(h, C.byref(d), C.byref(ka), C.byref(kw)))
+        k = d.k
+        arr = lambda p, t, n: np.ctypeslib.as_array((t * n).from_address(p)).copy()  # noqa: E731
+        e_x = arr(d.ext_x, C.c_int64, k)
+        px = FlattenPlan.from_extensions(d.t_x, e_x, d.block_x)
+        e_w = arr(d.ext_w, C.c_int64, px.padded_width)
+        pw = FlattenPlan.from_extensions(d.t_w, e_w, d.block_w)
+        cfg = LayerQuantConfig(bits=d.bits, smooth_scales=arr(d.smooth_scales, C.c_double, k),
+                               plan_x=px, plan_w=pw, act_scale=d.act_scale, weight=w)
+        info = {"kl_ratio_act": ka.value, "kl_ratio_w": kw.value, "w_scale": d.w_scale}
+        cfg.extra.update(info)
+        return cfg, info
+    finally:
+        lib().fqg_recipe_free(h)
+
+
+class Model:
+    """Recipe JSON + FQTA quantized archive -> device layers (the CLI's
+    load_recipes, flattenquant_cli.cpp:241-252); ``infer`` is cmd_infer
+    (flattenquant_cli.cpp:254-281) on archives. device < 0: parse only."""
+
+    def __init__(self, recipe_path: str, qmodel_path: Optional[str], device: int = 0,
+                 a_format: int = I8):
+        h = C.c_void_p()
+        check(lib().fqg_model_load(recipe_path.encode(),
+                                   qmodel_path.encode() if qmodel_path else None, device,
+                                   a_format, C.byref(h)))
+        self._h = h
+        n = C.c_int64()
+        check(lib().fqg_model_num_layers(h, C.byref(n)))
+        self.names = []
+        for i in range(n.value):
+            buf = C.create_string_buffer(1024)
+            check(lib().fqg_model_layer_name(h, i, buf, 1024))
+            self.names.append(buf.value.decode())
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().fqg_model_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    def recipe(self, i: int) -> dict:
+        """The parsed recipe of layer i (plain numpy copies)."""
+        d = _lib.LayerDesc()
+        ka, kw = C.c_double(), C.c_double()
+        check(lib().fqg_model_layer_recipe(self._h, i, C.byref(d), C.byref(ka), C.byref(kw)))
+        k = d.k
+        c1 = -(-(k + int(np.ctypeslib.as_array((C.c_int64 * k).from_address(d.ext_x)).sum()))
+               // d.block_x) * d.block_x
+        arr = lambda p, t, n: np.ctypeslib.as_array((t * n).from_address(p)).copy()  # noqa: E731
+        out = {"bits": d.bits, "k": k, "n": d.n, "s": arr(d.smooth_scales, C.c_double, k),
+               "t_x": d.t_x, "e_x": arr(d.ext_x, C.c_int64, k), "block_x": d.block_x,
+               "t_w": d.t_w, "e_w": arr(d.ext_w, C.c_int64, c1), "block_w": d.block_w,
+               "act_scale": d.act_scale, "w_scale": d.w_scale, "kl_ratio_act": ka.value,
+               "kl_ratio_w": kw.value}
+        if d.weight_q:
+            kp = -(-(c1 + int(out["e_w"].sum())) // d.block_w) * d.block_w
+            out["weight_q"] = arr(d.weight_q, C.c_int32, kp * d.n).reshape(kp, d.n)
+        return out
+
+    def infer(self, input_path: str, out_path: str) -> tuple[int, int]:
+        """-> (saturated elements, tensors run)."""
+        sat, ran = C.c_int64(), C.c_int64()
+        check(lib().fqg_model_infer(self._h, input_path.encode(), out_path.encode(),
+                                    C.byref(sat), C.byref(ran)))
+        return sat.value, ran.value
 
 
 def run_layer(cfg: LayerQuantConfig, x, device: int = 0) -> tuple[np.ndarray, int]:

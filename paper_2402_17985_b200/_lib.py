@@ -102,6 +102,11 @@ class GemmPlan(C.Structure):
     _fields_ = [("kernel", INT), ("tile_m", INT), ("tile_n", INT), ("splits", INT), ("ctas", INT)]
 
 
+class QuantOptions(C.Structure):
+    _fields_ = [("mode", INT), ("alpha", F64_), ("beta", F64_), ("gamma", F64_), ("block", I64),
+                ("bins", I64), ("smooth", INT), ("clip", INT)]
+
+
 # Every symbol include/fqg.h declares, with its ctypes signature.
 SIGNATURES = {
     "fqg_last_error": (C.c_char_p, []),
@@ -120,6 +125,18 @@ SIGNATURES = {
     "fqg_gemm_plan": (INT, [I64, I64, I64, INT, INT, INT, C.POINTER(GemmPlan)]),
     "fqg_shard_bounds": (INT, [I64, INT, INT, C.POINTER(I64), C.POINTER(I64), C.POINTER(I64)]),
     "fqg_layer_forward_sharded": (INT, [P, P, INT, I64, P, INT, INT, INT, P, INT, P, P, P, P]),
+    "fqg_quant_options_default": (None, [C.POINTER(QuantOptions)]),
+    "fqg_calibrate": (INT, [P, I64, I64, P, I64, I64, C.POINTER(QuantOptions), INT, C.POINTER(P)]),
+    "fqg_recipe_get": (INT, [P, C.POINTER(LayerDesc), C.POINTER(F64_), C.POINTER(F64_)]),
+    "fqg_recipe_free": (INT, [P]),
+    "fqg_model_load": (INT, [C.c_char_p, C.c_char_p, INT, INT, C.POINTER(P)]),
+    "fqg_model_destroy": (INT, [P]),
+    "fqg_model_num_layers": (INT, [P, C.POINTER(I64)]),
+    "fqg_model_layer_name": (INT, [P, I64, C.c_char_p, I64]),
+    "fqg_model_layer_recipe": (INT, [P, I64, C.POINTER(LayerDesc), C.POINTER(F64_),
+                                     C.POINTER(F64_)]),
+    "fqg_model_layer": (INT, [P, C.c_char_p, C.POINTER(P)]),
+    "fqg_model_infer": (INT, [P, C.c_char_p, C.c_char_p, C.POINTER(I64), C.POINTER(I64)]),
     "fqg_hash64": (C.c_uint64, [P, C.c_size_t, C.c_uint64]),
     "fqg_build_flatten_plan": (INT, [P, I64, F64_, I64, P, P, C.POINTER(I64), C.POINTER(I64)]),
     "fqg_split_against_threshold": (None, [F64_, F64_, C.POINTER(I64), C.POINTER(F64_)]),

@@ -594,7 +594,9 @@ struct PairLayout {
     // epilogue warp groups (4 warps each): NB = 2 drains its single accumulator
     // after the main loop with the unpack warps (or 4 spare warps) joining in
     // (4-byte outputs keep one group and the staged TMA-store epilogue instead)
-    static constexpr int epi_groups = (NB == 2 && EPIB != 32 * 32 * 4) ? (packed ? 3 : 4) : 1;
+    // (3 groups: 512 threads keep 128 registers per thread; a 4th group of spare
+    // warps for int8 operands spilled the 16-bit drain at 640 threads)
+    static constexpr int epi_groups = (NB == 2 && EPIB != 32 * 32 * 4) ? 3 : 1;
     // spare warps (after the unpack warps, if any) that only run epilogue groups
     static constexpr int spare_warps = (epi_groups - 1) * 4 - (packed && epi_groups > 1 ? unpack_warps : 0);
     static constexpr int threads = 256 + 32 * (unpack_warps + spare_warps);
