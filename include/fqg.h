@@ -195,7 +195,7 @@ typedef struct fqg_gemm_plan_info {
 int fqg_gemm_plan(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int y_dtype,
                   fqg_gemm_plan_info* out);
 
-/* fq::quantize_layer (pipeline.cpp:76-152) for modes O1/O2 with its scans on
+/* fq::quantize_layer (pipeline.cpp:76-152) for modes O1/O2/O3 with its scans on
  * the device: calibration channel maxima (collect_channel_maxes,
  * calibration.cpp:9-28), weight row maxima, and the KL bit-width selection
  * (select_bit_width, quantize.cpp:145-158: P / INT4 / INT8 round-trip
@@ -206,17 +206,19 @@ int fqg_gemm_plan(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int y_
  * desc.weight = W (the device weight tail computes the same weight_q).
  * weight: host f64 [k][n]; calib: host f64 [samples][rows][k]. */
 typedef struct fqg_quant_options {
-    int mode;            /* 1 = O1 (8 bits pinned), 2 = O2 (KL choice) */
+    int mode;            /* 1 = O1 (8 bits pinned), 2 = O2 (KL choice), 3 = O3 (O2 + GPTQ) */
     double alpha, beta, gamma;
     int64_t block, bins;
     int smooth, clip;
+    double damping;      /* O3: Hessian damping (hessian_from_calibration) */
 } fqg_quant_options;
 void fqg_quant_options_default(fqg_quant_options* o);  /* pipeline.hpp:24-34 */
 typedef struct fqg_recipe_s* fqg_recipe_t;
 int fqg_calibrate(const double* weight, int64_t k, int64_t n, const double* calib, int64_t samples,
                   int64_t rows, const fqg_quant_options* options, int device, fqg_recipe_t* out);
-/* The recipe as a layer description (arrays owned by the recipe; weight and
- * weight_q are NULL: set desc.weight = W before fqg_layer_create). */
+/* The recipe as a layer description (arrays owned by the recipe). O1/O2:
+ * weight_q is NULL, set desc.weight = W before fqg_layer_create. O3: weight_q
+ * is the GPTQ result (gptq.cpp:106-161, computed on the device). */
 int fqg_recipe_get(fqg_recipe_t recipe, fqg_layer_desc* desc, double* kl_ratio_act,
                    double* kl_ratio_w);
 int fqg_recipe_free(fqg_recipe_t recipe);

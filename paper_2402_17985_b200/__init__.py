@@ -317,8 +317,14 @@ def calibrate(weight, calib, mode: int = 2, device: int = 0, **opts):
         px = FlattenPlan.from_extensions(d.t_x, e_x, d.block_x)
         e_w = arr(d.ext_w, C.c_int64, px.padded_width)
         pw = FlattenPlan.from_extensions(d.t_w, e_w, d.block_w)
-        cfg = LayerQuantConfig(bits=d.bits, smooth_scales=arr(d.smooth_scales, C.c_double, k),
-                               plan_x=px, plan_w=pw, act_scale=d.act_scale, weight=w)
+        if d.weight_q:  # O3: the device GPTQ weight_q
+            wq = arr(d.weight_q, C.c_int32, pw.padded_width * d.n).reshape(pw.padded_width, d.n)
+            cfg = LayerQuantConfig(bits=d.bits, smooth_scales=arr(d.smooth_scales, C.c_double, k),
+                                   plan_x=px, plan_w=pw, act_scale=d.act_scale, weight_q=wq,
+                                   w_scale=d.w_scale)
+        else:
+            cfg = LayerQuantConfig(bits=d.bits, smooth_scales=arr(d.smooth_scales, C.c_double, k),
+                                   plan_x=px, plan_w=pw, act_scale=d.act_scale, weight=w)
         info = {"kl_ratio_act": ka.value, "kl_ratio_w": kw.value, "w_scale": d.w_scale}
         cfg.extra.update(info)
         return cfg, info

@@ -104,7 +104,7 @@ class GemmPlan(C.Structure):
 
 class QuantOptions(C.Structure):
     _fields_ = [("mode", INT), ("alpha", F64_), ("beta", F64_), ("gamma", F64_), ("block", I64),
-                ("bins", I64), ("smooth", INT), ("clip", INT)]
+                ("bins", I64), ("smooth", INT), ("clip", INT), ("damping", F64_)]
 
 
 # Every symbol include/fqg.h declares, with its ctypes signature.

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "fqg_internal.h"
+#include "gptq.h"
 #include "host.h"
 #include "split.cuh"
 
@@ -154,6 +155,17 @@ __global__ void __launch_bounds__(kThreads) k_src_hist(Src src, int64_t rows, do
         if (sh[i]) atomicAdd(hist + i, static_cast<unsigned long long>(sh[i]));
 }
 
+// The tensor itself, row-major (the O3 path's GEMM-like operands).
+template <class Src>
+__global__ void __launch_bounds__(kThreads) k_src_materialize(Src src, int64_t rows,
+                                                              double* __restrict__ out) {
+    bool over = false;
+    const int64_t total = rows * src.cols;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(kThreads) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * kThreads)
+        out[i] = src(i / src.cols, i % src.cols, over);
+}
+
 int grid_for(int64_t work, int sms) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + kThreads - 1) / kThreads,
                                                                     8LL * sms)));
@@ -234,6 +246,7 @@ struct fqg_recipe_s {
     std::vector<double> s;
     double t_x = 0, t_w = 0, act_scale = 0, w_scale = 0, kl_act = 0, kl_w = 0;
     std::vector<int64_t> e_x, e_w;
+    std::vector<int32_t> weight_q;  // O3: GPTQ weight_q [K'][N]
 };
 
 using namespace fqg;
@@ -242,7 +255,7 @@ extern "C" {
 
 void fqg_quant_options_default(fqg_quant_options* o) {
     // pipeline.hpp:24-34 (QuantOptions)
-    *o = fqg_quant_options{2, 0.5, 1.3, 1.86, 32, 2048, 1, 1};
+    *o = fqg_quant_options{2, 0.5, 1.3, 1.86, 32, 2048, 1, 1, 0.01};
 }
 
 int fqg_calibrate(const double* weight, int64_t k, int64_t n, const double* calib, int64_t samples,
@@ -251,7 +264,7 @@ int fqg_calibrate(const double* weight, int64_t k, int64_t n, const double* cali
         require(weight && calib && o && out, "calibrate: null argument");
         require(k >= 1 && n >= 1 && samples >= 1 && rows >= 1,
                 "quantize_layer: empty calibration set");
-        require(o->mode == 1 || o->mode == 2, "calibrate: mode must be O1 (1) or O2 (2)");
+        require(o->mode >= 1 && o->mode <= 3, "calibrate: mode must be O1 (1), O2 (2) or O3 (3)");
         require(o->gamma >= 0.0, "select_bit_width: gamma must be >= 0");
         require(o->bins >= 16, "build_histogram: bin_count < 16");
         int prev = -1;
@@ -336,6 +349,24 @@ int fqg_calibrate(const double* weight, int64_t k, int64_t n, const double* cali
         r->act_scale = r->t_x / qmax;
         if (mx_w == 0.0) throw Error(FQG_ERR_RUNTIME, "quantize_layer: weight is all zero");
         r->w_scale = mx_w / qmax;
+        if (o->mode == 3) {  // :144-147 gptq_optimize(w_flat, hessian_from_calibration(flat acts))
+            require(g.kp * g.kp <= (int64_t{1} << 31), "calibrate O3: K' too large for the Hessian");
+            double* xf = nullptr;
+            double* wf = nullptr;
+            int32_t* qd = nullptr;
+            FQG_CUDA(cudaMalloc(&xf, static_cast<size_t>(m * g.kp) * 8));
+            keep.push_back(xf);
+            FQG_CUDA(cudaMalloc(&wf, static_cast<size_t>(g.kp * n) * 8));
+            keep.push_back(wf);
+            FQG_CUDA(cudaMalloc(&qd, static_cast<size_t>(g.kp * n) * 4));
+            keep.push_back(qd);
+            k_src_materialize<ActSrc><<<grid_for(m * g.kp, sms), kThreads>>>(as, m, xf);
+            k_src_materialize<WgtSrc><<<grid_for(g.kp * n, sms), kThreads>>>(ws, g.kp, wf);
+            FQG_CUDA(cudaGetLastError());
+            gptq_weight_q(xf, m, static_cast<int>(g.kp), wf, n, o->damping, r->w_scale, qmax, qd);
+            r->weight_q.resize(static_cast<size_t>(g.kp * n));
+            FQG_CUDA(cudaMemcpy(r->weight_q.data(), qd, r->weight_q.size() * 4, cudaMemcpyDeviceToHost));
+        }
         *out = r.release();
     });
 }
@@ -356,6 +387,7 @@ int fqg_recipe_get(fqg_recipe_t r, fqg_layer_desc* d, double* kl_ratio_act, doub
         d->block_w = r->block;
         d->act_scale = r->act_scale;
         d->w_scale = r->w_scale;
+        d->weight_q = r->weight_q.empty() ? nullptr : r->weight_q.data();
         d->n_total = r->n;
         d->a_format = FQG_I8;
         d->b_format = r->bits == 4 ? FQG_I4 : FQG_I8;

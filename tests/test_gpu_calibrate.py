@@ -49,3 +49,24 @@ def test_calibrate_options_and_errors(ref, fq):
         assert cfg.plan_x.threshold == rl.info.T_x
     with pytest.raises(fq.FqgInvalidArgument):
         fq.calibrate(w, calib, mode=2, bins=8)
+
+
+@pytest.mark.parametrize("idx,k,n,rows,samples,bits_gamma", [(5, 96, 64, 32, 4, 1e6),
+                                                              (6, 160, 96, 48, 2, 0.5),
+                                                              (7, 256, 128, 64, 3, 1e6)])
+def test_o3_gptq_weight_q_equals_reference(ref, fq, idx, k, n, rows, samples, bits_gamma):
+    """O3 (gptq.cpp:73-161) on the device: Hessian, Cholesky, inverse factor and
+    the blocked column updates keep the reference's per-element FP64 sequences,
+    so weight_q is identical."""
+    w, calib, x, _ = ref.synthetic_layer(idx, in_channels=k, out_channels=n, rows=rows,
+                                         samples=samples)
+    rl = ref.quantize_layer(w, calib, mode=3, gamma=bits_gamma)
+    L = rl.to_layer()
+    cfg, info = fq.calibrate(w, calib, mode=3, gamma=bits_gamma)
+    assert cfg.bits == L.bits and info["w_scale"] == L.s_w
+    bad = np.argwhere(cfg.weight_q != L.wq)
+    assert bad.size == 0, f"{len(bad)} weight_q mismatches, first {tuple(bad[0])}"
+    layer = fq.Layer(cfg, b_format=fq.I4 if cfg.bits == 4 else fq.I8)
+    y_ref, sat_ref = rl.run_layer(x)
+    y, sat = layer.run_layer(x)
+    assert np.array_equal(y, y_ref) and sat == sat_ref
