@@ -92,10 +92,9 @@ int fqg_gemm_plan(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int y_
     return guard([&] {
         require(out != nullptr && m >= 1 && n >= 1 && kp >= 1, "fqg_gemm_plan: bad argument");
         require(dtype_size(y_dtype) > 0 && y_dtype != FQG_I8, "fqg_gemm_plan: bad output dtype");
-        (void)b_fmt;  // the choice depends on the shape and the activation format only
         int dev = 0;
         FQG_CUDA(cudaGetDevice(&dev));
-        const GemmPlan p = plan_gemm(m, n, kp, a_fmt, FQG_I8, 0, num_sms(dev));
+        const GemmPlan p = plan_gemm(m, n, kp, a_fmt, b_fmt, 0, num_sms(dev));
         *out = {p.kernel, p.tile_m, p.tile_n, p.splits, p.ctas};
     });
 }

@@ -87,13 +87,19 @@ GemmPlan plan_gemm(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int v
     const int64_t num_kb = (kp + BK - 1) / BK;
     if (v == 2) {
         p.kernel = 2;
-        p.tile_m = 2 * BM;
         // 256 x 512 tiles (NB = 2) need enough tiles to fill the CTA pairs;
         // otherwise 256 x 256 (plus split-K when even those are few).
         const int64_t t2 = ((m + 255) / 256) * ((n + 511) / 512);
-        const int nb = nb_env ? nb_env : (n >= 512 && t2 >= 48 ? 2 : 1);
-        p.tile_n = 256 * nb;
-        const int64_t tiles = ((m + 255) / 256) * ((n + p.tile_n - 1) / p.tile_n);
+        int nb = nb_env ? nb_env : (n >= 512 && t2 >= 48 ? 2 : 1);
+        // Packed (int4) weights: 512 x 256 tiles (nb = 3) instead of 256 x 512, which
+        // halve the expanded B tile per MAC (the int4 main loop is bound by shared-
+        // memory bandwidth, gemm_kernels.cuh PairLayout).
+        const bool packed_b = b_fmt == FQG_I4 || b_fmt == FQG_I4_BIASED;
+        const int64_t t3 = ((m + 511) / 512) * ((n + 255) / 256);
+        if (!nb_env && nb == 2 && packed_b && m >= 512 && t3 >= 48) nb = 3;
+        p.tile_m = nb == 3 ? 512 : 2 * BM;
+        p.tile_n = nb == 3 ? 256 : 256 * nb;
+        const int64_t tiles = ((m + p.tile_m - 1) / p.tile_m) * ((n + p.tile_n - 1) / p.tile_n);
         const int64_t pairs = std::max(1, sms / 2);
         // Split-K for small M: fewer than half the pairs would have a tile.
         if (nb == 1 && 2 * tiles <= pairs && num_kb >= 8) {

@@ -569,19 +569,27 @@ __device__ unsigned long long g_dbg2[296][8];  // pair packed path: see launch_p
 // double-buffered accumulator; NB = 2 -> 256 x 512 tiles, two accumulators
 // filling TMEM (no double buffer): the A tile is read once per two MMAs, so
 // L2 -> SMEM bytes per MAC drop by a quarter (the kernel is TMA-throughput bound).
+// NB = 3 encodes 512 x 256 tiles (MB = 2 row sub-tiles, one 256-column B block):
+// two MMAs per K step with different A and the same B, so the expanded B tile
+// (the costly one with packed weights: TMA write, unpack read, unpack write,
+// MMA read) is half as large per MAC as with 256 x 512, at the price of a
+// second A sub-tile; shared-memory traffic per k-block and CTA drops from 144 KB
+// to 128 KB for int8 A / packed B (the int4 main loop is SMEM-bandwidth bound).
 template <int STAGES, bool APK, bool BPK, int NB = 1, int EPIB = 0>
 struct PairLayout {
     static constexpr int BN = 256;
-    static constexpr int NACC = NB == 1 ? 2 : 1;  // accumulator buffers
+    static constexpr int NBS = NB == 3 ? 1 : NB;   // 256-column B blocks per tile
+    static constexpr int MBS = NB == 3 ? 2 : 1;    // 256-row A sub-tiles per tile
+    static constexpr int NACC = NBS * MBS == 1 ? 2 : 1;  // accumulator buffers
     static constexpr bool packed = APK || BPK;
-    static constexpr int a_raw = APK ? BM * BK / 2 : BM * BK;       // own 128 rows of A
-    static constexpr int b_raw = NB * (BPK ? (BN / 2) * BK / 2 : (BN / 2) * BK);  // own halves of B
+    static constexpr int a_raw = MBS * (APK ? BM * BK / 2 : BM * BK);  // own 128 rows per sub-tile
+    static constexpr int b_raw = NBS * (BPK ? (BN / 2) * BK / 2 : (BN / 2) * BK);  // own halves of B
     static constexpr int raw_stage = a_raw + b_raw;
     static constexpr int direct_bytes = (APK ? 0 : a_raw) + (BPK ? 0 : b_raw);
     static constexpr int packed_bytes = (APK ? a_raw : 0) + (BPK ? b_raw : 0);
     static constexpr int USTAGES = packed ? (NB == 1 ? 4 : 3) : 0;
-    static constexpr int a_unp = APK ? BM * BK : 0;
-    static constexpr int b_unp = BPK ? NB * (BN / 2) * BK : 0;
+    static constexpr int a_unp = APK ? MBS * BM * BK : 0;
+    static constexpr int b_unp = BPK ? NBS * (BN / 2) * BK : 0;
     static constexpr int unp_stage = a_unp + b_unp;
     static constexpr int unp_off = STAGES * raw_stage;
     // epilogue staging: per epilogue warp 2 buffers of a 32 x 32 output block
@@ -596,11 +604,11 @@ struct PairLayout {
     // (4-byte outputs keep one group and the staged TMA-store epilogue instead)
     // (3 groups: 512 threads keep 128 registers per thread; a 4th group of spare
     // warps for int8 operands spilled the 16-bit drain at 640 threads)
-    static constexpr int epi_groups = (NB == 2 && EPIB != 32 * 32 * 4) ? 3 : 1;
+    static constexpr int epi_groups = (NBS * MBS == 2 && EPIB != 32 * 32 * 4) ? 3 : 1;
     // spare warps (after the unpack warps, if any) that only run epilogue groups
     static constexpr int spare_warps = (epi_groups - 1) * 4 - (packed && epi_groups > 1 ? unpack_warps : 0);
     static constexpr int threads = 256 + 32 * (unpack_warps + spare_warps);
-    static constexpr int tmem_cols = NB == 1 ? 2 * BN : NB * BN;
+    static constexpr int tmem_cols = NACC == 2 ? 2 * BN : NBS * MBS * BN;
     // Arrivals freeing a raw stage in each CTA: the leader's multicast MMA
     // commit when an operand is read straight from the raw stage, plus one per
     // local unpack warp that reads it.
@@ -632,7 +640,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     using OT = typename OutT<OUT>::T;
     constexpr int NACC = L::NACC;
     constexpr int NG = L::epi_groups;
-    constexpr int TN = NB * L::BN;  // tile columns
+    constexpr int NBS = L::NBS, MBS = L::MBS;
+    constexpr int TN = NBS * L::BN;     // tile columns
+    constexpr int TM = MBS * 2 * BM;    // tile rows
     const long long t_start = clock64();
     unsigned long long gstart = 0;
     if (dbg) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gstart));
@@ -653,7 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
-    const int num_m = (m + 2 * BM - 1) / (2 * BM);
+    const int num_m = (m + TM - 1) / TM;
     const int num_n = (n + TN - 1) / TN;
     const int num_tiles = num_m * num_n;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -743,48 +753,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                 asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ge0));
                 atomicAdd(&g_dbg2[blockIdx.x % 296][6], ge0 - gstart);  // tfull reached (ns)
             }
-            const int rloc = rank * BM + ew * 32 + lane;  // row within the 256-row tile
-            const int row = m_blk * 2 * BM + rloc;
+#pragma unroll 1
+            for (int sub = 0; sub < MBS; ++sub) {  // 256-row sub-tiles (NB = 3: two)
+            const int rloc = rank * BM + ew * 32 + lane;  // row within the 256-row sub-tile
+            const int row = m_blk * TM + sub * 2 * BM + rloc;
             const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+            const uint32_t t_row =
+                tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + sub * BN;
             // 2-byte outputs, no bias, full tile: 16-column chunks with the next
             // chunk's TMEM load in flight while this one is converted and stored
             constexpr bool OUT16 = OUT == FQG_F16 || OUT == FQG_BF16;
             if (OUT16 && !plane && bias == nullptr && (vec_ok & 2) && !(dbg & 12) &&
                 (n_blk + 1) * TN <= n) {
+                // one pipelined stream over the chunks of every sub-tile: chunk cc is
+                // sub-tile cc / NCH (whose accumulator columns follow contiguously)
+                if (sub > 0) continue;
                 const int mode = cvt_mode(small_acc, s32);
                 constexpr int NCH = TN / 16;
+                constexpr int NCHT = MBS * NCH;
+                static_assert(MBS == 1 || TN == BN, "sub-tile accumulators must be contiguous");
+                // row-sum corrections of this lane's rows in sub-tiles 0 and 1
+                const int32_t corr1 = (MBS > 1 && BF == FU4 && row + 2 * BM < m)
+                                          ? 8 * rowsum[row + 2 * BM] : 0;
                 uint32_t dsink = 0;  // debug bits 32/64 (drain anatomy experiments)
-                auto emit = [&](uint32_t (&rr)[16], int c) {
+                auto emit = [&](uint32_t (&rr)[16], int cc) {
+                    const int sb = MBS == 1 ? 0 : cc / NCH, c = MBS == 1 ? cc : cc % NCH;
+                    const int rs = row + sb * 2 * BM;
                     uint32_t pk[8];
                     if (dbg & 32) {
 #pragma unroll
                         for (int q = 0; q < 8; ++q) pk[q] = rr[2 * q] ^ (rr[2 * q + 1] << 1);
                     } else {
-                        cvt16_certified<OUT, 16>(rr, corr, s32, s, mode, pk);
+                        cvt16_certified<OUT, 16>(rr, sb ? corr1 : corr, s32, s, mode, pk);
                     }
                     if (dbg & 64) {
 #pragma unroll
                         for (int q = 0; q < 8; ++q) dsink ^= pk[q];
-                    } else if (row < m) {  // 32 contiguous bytes: one full sector per lane
-                        stg256(static_cast<uint16_t*>(y) + static_cast<int64_t>(row) * ldy +
+                    } else if (rs < m) {  // 32 contiguous bytes: one full sector per lane
+                        stg256(static_cast<uint16_t*>(y) + static_cast<int64_t>(rs) * ldy +
                                    n_blk * TN + c * 16,
                                pk);
                     }
                 };
                 uint32_t ra[16], rb[16];
                 int c = grp;
-                if (c < NCH) ptx::tmem_ld_32x32b_x16(t_row + c * 16, ra);
+                if (c < NCHT) ptx::tmem_ld_32x32b_x16(t_row + c * 16, ra);
                 ptx::tmem_wait_ld_r(ra);
 #pragma unroll 1
-                while (c < NCH) {
+                while (c < NCHT) {
                     const int c1 = c + ng;
-                    if (c1 < NCH) ptx::tmem_ld_32x32b_x16(t_row + c1 * 16, rb);
+                    if (c1 < NCHT) ptx::tmem_ld_32x32b_x16(t_row + c1 * 16, rb);
                     emit(ra, c);
                     ptx::tmem_wait_ld_r(rb);
-                    if (c1 >= NCH) break;
+                    if (c1 >= NCHT) break;
                     const int c2 = c1 + ng;
-                    if (c2 < NCH) ptx::tmem_ld_32x32b_x16(t_row + c2 * 16, ra);
+                    if (c2 < NCHT) ptx::tmem_ld_32x32b_x16(t_row + c2 * 16, ra);
                     emit(rb, c1);
                     ptx::tmem_wait_ld_r(ra);
                     c = c2;
@@ -846,7 +869,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                         ptx::fence_proxy_async_smem();
                         __syncwarp();
                         if (lane == 0) {
-                            ptx::tma_store_2d(&tmY, ep, col0, m_blk * 2 * BM + rank * BM + ew * 32);
+                            ptx::tma_store_2d(&tmY, ep, col0,
+                                              m_blk * TM + sub * 2 * BM + rank * BM + ew * 32);
                             ptx::bulk_commit();
                         }
                         continue;
@@ -863,6 +887,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                                          corr, s32, cvt_mode(small_acc, s32));
                 }
             }
+            }  // sub-tiles
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0 && (HELP_ALL || grp == 0))
@@ -886,7 +911,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
         uint32_t phase = 0;
         for_each_seg([&](int tile, int kb0, int kb1, int) {
             const int m_blk = tile % num_m, n_blk = tile / num_m;
-            const int a_row = m_blk * 2 * BM + rank * BM;
+            const int a_row = m_blk * TM + rank * BM;         // + mb * 2 BM per sub-tile
             const int b_row = n_blk * TN + rank * (BN / 2);  // + nb * BN per block
             for (int kb = kb0; kb < kb1; ++kb) {
                 ptx::mbar_wait(&empty[stage], phase ^ 1);
@@ -898,17 +923,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                 }
                 if constexpr (L::packed_bytes > 0)
                     ptx::mbar_arrive_expect_tx(&full_unp[stage], L::packed_bytes);
-                if constexpr (APK)
-                    ptx::tma_load_2d_hint(sa, &tmA, &full_unp[stage], kb * BK / 2, a_row, keep);
-                else
-                    ptx::tma_load_2d_2sm(sa, &tmA, lead_full, kb * BK, a_row, keep);
 #pragma unroll
-                for (int nb = 0; nb < NB; ++nb) {
+                for (int mb = 0; mb < MBS; ++mb) {
+                    if constexpr (APK)
+                        ptx::tma_load_2d_hint(sa + mb * (L::a_raw / MBS), &tmA, &full_unp[stage],
+                                              kb * BK / 2, a_row + mb * 2 * BM, keep);
+                    else
+                        ptx::tma_load_2d_2sm(sa + mb * (L::a_raw / MBS), &tmA, lead_full, kb * BK,
+                                             a_row + mb * 2 * BM, keep);
+                }
+#pragma unroll
+                for (int nb = 0; nb < NBS; ++nb) {
                     if constexpr (BPK)
-                        ptx::tma_load_2d_hint(sb + nb * (L::b_raw / NB), &tmB, &full_unp[stage],
+                        ptx::tma_load_2d_hint(sb + nb * (L::b_raw / NBS), &tmB, &full_unp[stage],
                                               kb * BK / 2, b_row + nb * BN, keep);
                     else
-                        ptx::tma_load_2d_2sm(sb + nb * (L::b_raw / NB), &tmB, lead_full, kb * BK,
+                        ptx::tma_load_2d_2sm(sb + nb * (L::b_raw / NBS), &tmB, lead_full, kb * BK,
                                              b_row + nb * BN, keep);
                 }
                 if (++stage == STAGES) {
@@ -944,10 +974,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
 #pragma unroll
                 for (int k = 0; k < BK / UK; ++k) {
 #pragma unroll
-                    for (int nb = 0; nb < NB; ++nb)
-                        ptx::mma_i8_pair(d_tmem + nb * BN, ptx::smem_desc_sw128_kmajor(a_addr + k * UK),
-                                         ptx::smem_desc_sw128_kmajor(b_addr + nb * ((BN / 2) * BK) + k * UK),
-                                         idesc, (kb != kb0 || k != 0) ? 1u : 0u);
+                    for (int mb = 0; mb < MBS; ++mb)
+#pragma unroll
+                        for (int nb = 0; nb < NBS; ++nb)
+                            ptx::mma_i8_pair(d_tmem + (mb * NBS + nb) * BN,
+                                             ptx::smem_desc_sw128_kmajor(a_addr + mb * (BM * BK) + k * UK),
+                                             ptx::smem_desc_sw128_kmajor(b_addr + nb * ((BN / 2) * BK) + k * UK),
+                                             idesc, (kb != kb0 || k != 0) ? 1u : 0u);
                 }
                 if constexpr (L::direct_bytes > 0) ptx::mma_commit_pair(&empty[stage], 0x3);
                 if constexpr (L::packed) {
@@ -1003,9 +1036,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                 long long tw2 = d0 ? clock64() : 0;
                 const uint8_t* raw = smem + stage * L::raw_stage;
                 uint8_t* unp = smem + L::unp_off + us * L::unp_stage;
-                if constexpr (APK) unpack_tile<AF>(raw, unp, BM, utid, nut);
+                if constexpr (APK) unpack_tile<AF>(raw, unp, MBS * BM, utid, nut);
                 if constexpr (BPK)
-                    unpack_tile<BF>(raw + L::a_raw, unp + L::a_unp, NB * (BN / 2), utid, nut);
+                    unpack_tile<BF>(raw + L::a_raw, unp + L::a_unp, NBS * (BN / 2), utid, nut);
                 if (d0) {
                     atomicAdd(&g_dbg2[blockIdx.x % 296][2], tw1 - tw0);
                     atomicAdd(&g_dbg2[blockIdx.x % 296][3], tw2 - tw1);
@@ -1283,6 +1316,7 @@ void dispatch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t s) {
             default: throw Error(FQG_ERR_INVALID, "gemm: unsupported output dtype");
         }
     };
+    if (p.tile_m == 512) return go(std::integral_constant<int, 3>{});
     if (p.tile_n == 512) return go(std::integral_constant<int, 2>{});
     return go(std::integral_constant<int, 1>{});
 }

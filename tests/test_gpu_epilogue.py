@@ -23,7 +23,9 @@ PATHS = {  # name: (M, N, K', expected plan {kernel, tile_n, splits>1})
     "pair_256x256": (1024, 2560, 512, (2, 256, False)),
     "pair_256x512": (2048, 3072, 256, (2, 512, False)),
     "splitk_reduce": (256, 1024, 2048, (2, 256, True)),
+    "pair_512x256_int4_weights": (2048, 3072, 256, (2, 256, False)),  # packed B: 512-row tiles
 }
+PACKED_B = {"pair_512x256_int4_weights"}
 OUTS = ["f16", "bf16", "f32", "f64"]
 BIASES = [None, "f64", "f32", "f16", "bf16"]
 
@@ -60,8 +62,15 @@ def test_epilogue_out_and_bias(fq, path):
     m, n, kp, (kern, tile_n, split) = PATHS[path]
     g = torch.Generator().manual_seed(m * 7 + n)
     a = torch.randint(-127, 128, (m, kp), dtype=torch.int8, generator=g)
-    b = torch.randint(-127, 128, (n, kp), dtype=torch.int8, generator=g)
+    packed = path in PACKED_B
+    b = torch.randint(-7 if packed else -127, 8 if packed else 128, (n, kp), dtype=torch.int8,
+                      generator=g)
     acc = a.numpy().astype(np.int64) @ b.numpy().astype(np.int64).T
+    if packed:  # FQG_I4: per group of 32 k, byte i = q[i] & 15 | q[16 + i] << 4
+        nib = (b.numpy().astype(np.int32) & 15).reshape(n, kp // 32, 2, 16)
+        b = torch.from_numpy((nib[:, :, 0, :] | (nib[:, :, 1, :] << 4)).astype(np.uint8)
+                             .reshape(n, kp // 2).view(np.int8))
+    b_code, ldb = (_lib.I4, kp // 2) if packed else (_lib.I8, kp)
     sx, sw = 3.7e-5, 0.0123
     s = sx * sw  # quantize.cpp:193, formed once in f64
     scale = torch.tensor([sx, sw], dtype=torch.float64, device="cuda")
@@ -71,8 +80,10 @@ def test_epilogue_out_and_bias(fq, path):
     code = {"f16": _lib.F16, "bf16": _lib.BF16, "f32": _lib.F32, "f64": _lib.F64}
     st = torch.cuda.current_stream().cuda_stream
     for out in OUTS:
-        p = plan(fq, m, n, kp, _lib.I8, _lib.I8, code[out])
+        p = plan(fq, m, n, kp, _lib.I8, b_code, code[out])
         assert p.kernel == kern, (path, out, p.kernel)
+        if packed:
+            assert p.tile_m == 512, (path, out, p.tile_m)
         if tile_n is not None:
             assert p.tile_n == tile_n, (path, out, p.tile_n)
         assert (p.splits > 1) == split, (path, out, p.splits)
@@ -85,7 +96,7 @@ def test_epilogue_out_and_bias(fq, path):
                 bias = bias_d.double().cpu().numpy()  # the bias values the device sees
             want = _round_out(acc.astype(np.float64) * s + bias[None, :], out)
             y = torch.empty((m, n), dtype=tdt[out], device="cuda")
-            fq.check(fq.lib().fqg_gemm(ad.data_ptr(), _lib.I8, kp, bd.data_ptr(), _lib.I8, kp, m,
+            fq.check(fq.lib().fqg_gemm(ad.data_ptr(), _lib.I8, kp, bd.data_ptr(), b_code, ldb, m,
                                        n, kp, y.data_ptr(), code[out], n, scale.data_ptr(),
                                        bias_d.data_ptr() if bias_d is not None else None,
                                        code[bias_dt] if bias_dt else _lib.NONE, st))
