@@ -153,9 +153,9 @@ __device__ __forceinline__ uint32_t pack_i4_word(uint32_t lo, uint32_t hi) {
 //               one 16-byte x load per row, the R rows' loads in flight
 //               together); certificate c_j / P_j loaded once per group and
 //               reused for the R rows; slot bytes go to the row buffers in SMEM.
-//               Tier-2 elements only set a bit in the row's SMEM bitmap.
+//               Tier-2 elements are queued (warp-aggregated SMEM atomics).
 //   2. splits   the "hot" channels (calibrated maximum >= 4 T_x: exact path on
-//               every row, from a per-layer list) and the bitmap's elements run
+//               every row, from a per-layer list) and the queued elements run
 //               the exact split of split.cuh: piece 0 into slot j and the run of
 //               extension pieces (count full +-q(T) pieces, then q(rem);
 //               flatten.cpp:71-72) into the channel's slots K + off_j ...
@@ -211,26 +211,23 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
     extern __shared__ __align__(16) uint8_t sm[];
     const int tid = threadIdx.x;
     const int k = p.k, kp = p.kp, c1 = p.c1, ldf = p.ldf;
-    const int ngrp = k >> 3, nbw = (ngrp + 3) >> 2;  // channel groups, bitmap words per row
+    const int ngrp = k >> 3;  // channel groups of 8
     const int row0 = blockIdx.x * R;
     const int nrow = min(R, p.m - row0);
     const SplitConsts& sc = p.sc;
     int8_t* const rows = reinterpret_cast<int8_t*>(sm);                     // [R][ldf]
-    uint32_t* const bitmap = reinterpret_cast<uint32_t*>(sm + R * ldf);      // [R][nbw]
-    uint8_t* const bitmap8 = reinterpret_cast<uint8_t*>(bitmap);
     __shared__ uint32_t list[kListCap];  // compacted tier-2 elements: r << 24 | j
     __shared__ int rsum_s[R];
     __shared__ int qlen;
     if (tid < R) rsum_s[tid] = 0;
     if (tid == 0) qlen = 0;
-    {  // zero the plan_x extension slots [K, C1), the tier-2 bitmap, and the byte
-       // at K' (plan_w padding copies read it)
+    {  // zero the plan_x extension slots [K, C1) and the byte at K' (plan_w padding
+       // copies read it)
         const int z0 = (k + 15) & ~15;
 #pragma unroll
         for (int r = 0; r < R; ++r)
             for (int u = tid; u < ((c1 - z0) >> 4); u += kThreads)
                 *reinterpret_cast<uint4*>(rows + r * ldf + z0 + 16 * u) = make_uint4(0u, 0u, 0u, 0u);
-        for (int u = tid; u < R * nbw; u += kThreads) bitmap[u] = 0u;
         if (tid < R) {
             if (z0 != k) *reinterpret_cast<uint2*>(rows + tid * ldf + k) = make_uint2(0u, 0u);
             rows[tid * ldf + kp] = 0;
@@ -243,53 +240,6 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
 #pragma unroll
     for (int r = 0; r < R; ++r) rs[r] = 0;
 
-    // ---- 1. tier 1: one FFMA per element; tier-2 elements set a bitmap bit ----
-    const uint4* xr[R];  // row pointers (rows past M read row M - 1 and are never stored)
-#pragma unroll
-    for (int r = 0; r < R; ++r)
-        xr[r] = static_cast<const uint4*>(p.x) + static_cast<int64_t>(min(row0 + r, p.m - 1)) * (p.ldx >> 3);
-    const float4* const cj4 = reinterpret_cast<const float4*>(p.cj);
-    const uint4* const pj4 = reinterpret_cast<const uint4*>(p.pj);
-    for (int g = tid; g < ngrp; g += kThreads) {
-        uint4 xw[R];
-#pragma unroll
-        for (int r = 0; r < R; ++r) xw[r] = __ldg(xr[r] + g);
-        const float4 ca = __ldg(cj4 + 2 * g);
-        const float4 cb = __ldg(cj4 + 2 * g + 1);
-        const uint4 pw = __ldg(pj4 + g);
-        const float cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-        const uint32_t pv[4] = {pw.x, pw.y, pw.z, pw.w};
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const uint32_t w[4] = {xw[r].x, xw[r].y, xw[r].z, xw[r].w};
-            uint32_t tw[4], bq[8];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                tw[e] = pv[e] - (w[e] & 0x7FFF7FFFu);
-                const float2 f = word_to_f32x2<F16>(w[e]);
-                bq[2 * e] = __float_as_uint(__fmaf_rn(f.x, cc[2 * e], kMagic));
-                bq[2 * e + 1] = __float_as_uint(__fmaf_rn(f.y, cc[2 * e + 1], kMagic));
-            }
-            const uint32_t wlo = pack_lowbytes(bq[0], bq[1], bq[2], bq[3]);
-            const uint32_t whi = pack_lowbytes(bq[4], bq[5], bq[6], bq[7]);
-            *reinterpret_cast<uint2*>(rows + r * ldf + 8 * g) = make_uint2(wlo, whi);
-            if (want_rs) {
-                rs[r] = __dp4a(static_cast<int>(wlo), 0x01010101, rs[r]);
-                rs[r] = __dp4a(static_cast<int>(whi), 0x01010101, rs[r]);
-            }
-            const uint32_t all = tw[0] & tw[1] & tw[2] & tw[3] & 0x80008000u;
-            if (all != 0x80008000u) {  // some element outside its certificate: tier 2
-                const uint32_t msk = ((~tw[0] >> 15) & 1u) | ((~tw[0] >> 30) & 2u) |
-                                     ((~tw[1] >> 13) & 4u) | ((~tw[1] >> 28) & 8u) |
-                                     ((~tw[2] >> 11) & 16u) | ((~tw[2] >> 26) & 32u) |
-                                     ((~tw[3] >> 9) & 64u) | ((~tw[3] >> 24) & 128u);
-                bitmap8[r * nbw * 4 + g] = static_cast<uint8_t>(msk);
-            }
-        }
-    }
-    __syncthreads();
-
-    // ---- 2. exact splits: hot channels on every row, then the bitmap ----
     unsigned long long sat = 0;
     const uint16_t* x16 = static_cast<const uint16_t*>(p.x);
     // piece 0 into slot j (replacing the tier-1 byte), pieces 1 .. E_j into the
@@ -314,34 +264,65 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         }
         return d;
     };
-    // the bitmap's elements as a dense list (ballot compaction, one SMEM atomic
-    // per warp), so the divergent exact path runs with full warps
-    for (int u0 = 0; u0 < nrow * nbw; u0 += kThreads) {
-        const int u = u0 + tid;
-        const uint32_t b = u < nrow * nbw ? bitmap[u] : 0u;
-        const int c = __popc(b);
-        int incl = c;
+    // ---- 1. tier 1: one FFMA per element; tier-2 elements are queued ----
+    // the block's rows as 32-bit offsets from its first row (rows past M read row
+    // M - 1 and are never stored)
+    const uint4* const xr0 = static_cast<const uint4*>(p.x) + static_cast<int64_t>(row0) * (p.ldx >> 3);
+    uint32_t xoff[R];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, incl, o);
-            if ((tid & 31) >= o) incl += v;
-        }
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        int base = 0;
-        if ((tid & 31) == 31 && total > 0) base = atomicAdd(&qlen, total);
-        base = __shfl_sync(0xffffffffu, base, 31) + incl - c;
-        if (c > 0) {
-            const int r = u / nbw, j0 = 32 * (u - r * nbw);
-            uint32_t bb = b;
-            while (bb != 0u) {
-                const int e = __ffs(static_cast<int>(bb)) - 1;
-                bb &= bb - 1u;
-                if (base < kListCap) list[base] = static_cast<uint32_t>(r << 24 | (j0 + e));
-                ++base;
+    for (int r = 0; r < R; ++r)
+        xoff[r] = static_cast<uint32_t>((min(row0 + r, p.m - 1) - row0) * (p.ldx >> 3));
+    const float4* const cj4 = reinterpret_cast<const float4*>(p.cj);
+    const uint4* const pj4 = reinterpret_cast<const uint4*>(p.pj);
+    for (int g = tid; g < ngrp; g += kThreads) {
+        uint4 xw[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) xw[r] = __ldg(xr0 + xoff[r] + g);
+        const float4 ca = __ldg(cj4 + 2 * g);
+        const float4 cb = __ldg(cj4 + 2 * g + 1);
+        const uint4 pw = __ldg(pj4 + g);
+        const float cc[8] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+        const uint32_t pv[4] = {pw.x, pw.y, pw.z, pw.w};
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const uint32_t w[4] = {xw[r].x, xw[r].y, xw[r].z, xw[r].w};
+            uint32_t tw[4], bq[8];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                tw[e] = pv[e] - (w[e] & 0x7FFF7FFFu);
+                const float2 f = word_to_f32x2<F16>(w[e]);
+                bq[2 * e] = __float_as_uint(__fmaf_rn(f.x, cc[2 * e], kMagic));
+                bq[2 * e + 1] = __float_as_uint(__fmaf_rn(f.y, cc[2 * e + 1], kMagic));
+            }
+            const uint32_t wlo = pack_lowbytes(bq[0], bq[1], bq[2], bq[3]);
+            const uint32_t whi = pack_lowbytes(bq[4], bq[5], bq[6], bq[7]);
+            *reinterpret_cast<uint2*>(rows + r * ldf + 8 * g) = make_uint2(wlo, whi);
+            // row sums unconditionally (two dp4a are cheaper than the branch)
+            rs[r] = __dp4a(static_cast<int>(wlo), 0x01010101, rs[r]);
+            rs[r] = __dp4a(static_cast<int>(whi), 0x01010101, rs[r]);
+            const uint32_t all = tw[0] & tw[1] & tw[2] & tw[3] & 0x80008000u;
+            if (all != 0x80008000u && row0 + r < p.m) {  // outside the certificate: tier 2
+                uint32_t msk = ((~tw[0] >> 15) & 1u) | ((~tw[0] >> 30) & 2u) |
+                               ((~tw[1] >> 13) & 4u) | ((~tw[1] >> 28) & 8u) |
+                               ((~tw[2] >> 11) & 16u) | ((~tw[2] >> 26) & 32u) |
+                               ((~tw[3] >> 9) & 64u) | ((~tw[3] >> 24) & 128u);
+                while (msk != 0u) {  // (the compiler aggregates the SMEM atomics per warp)
+                    const int e = __ffs(static_cast<int>(msk)) - 1;
+                    msk &= msk - 1u;
+                    const int j = 8 * g + e;
+                    const int slot = atomicAdd(&qlen, 1);
+                    if (slot < kListCap)
+                        list[slot] = static_cast<uint32_t>(r << 24 | j);
+                    else  // pathological input: run it here (this thread owns the group's bytes)
+                        rs[r] += split_store(r, j, __ldg(p.cap + j), __ldg(p.off + j),
+                                             __ldg(p.rs32 + j));
+                }
             }
         }
     }
     __syncthreads();
+
+    // ---- 2. exact splits: hot channels on every row, then the queued elements ----
     const int nhot_items = nrow * p.nhot;
     const int nlist = min(qlen, kListCap);
     for (int i = tid; i < nhot_items + nlist; i += kThreads) {
@@ -359,25 +340,6 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         const int d = split_store(r, j, cap_e, off_j, rs32_j);
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) rs[rr] += rr == r ? d : 0;
-    }
-    if (qlen > kListCap) {  // pathological input: the rest, straight from the bitmap
-        for (int u = tid; u < nrow * nbw; u += kThreads) {
-            uint32_t b = bitmap[u];
-            const int r = u / nbw, j0 = 32 * (u - r * nbw);
-            int dsum = 0;
-            while (b != 0u) {
-                const int e = __ffs(static_cast<int>(b)) - 1;
-                b &= b - 1u;
-                const int j = j0 + e;
-                bool listed = false;  // the first kListCap entries were processed above
-                for (int q = 0; q < kListCap && !listed; ++q)
-                    listed = list[q] == static_cast<uint32_t>(r << 24 | j);
-                if (!listed)
-                    dsum += split_store(r, j, __ldg(p.cap + j), __ldg(p.off + j), __ldg(p.rs32 + j));
-            }
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) rs[rr] += rr == r ? dsum : 0;
-        }
     }
     __syncthreads();
 
@@ -469,7 +431,7 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     if (rb_env == 1 || rb_env == 2 || rb_env == 4 || rb_env == 8) rb = rb_env;
     const int ldf = static_cast<int>((a.kp + 16 + 15) / 16 * 16);
     auto smem_of = [&](int r) {
-        return static_cast<size_t>(r) * ldf + static_cast<size_t>(r) * ((a.k / 8 + 3) / 4) * 4;
+        return static_cast<size_t>(r) * ldf;
     };
     while (rb > 1 && smem_of(rb) > 200 * 1024) rb >>= 1;
     const size_t smem = smem_of(rb);
