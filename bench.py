@@ -559,8 +559,8 @@ def main():
                 "pinned_host_buffers": {"value": ops / t_e2e_pinned / 1e12, "unit": "TOPS",
                                         "tokens_per_s": m / t_e2e_pinned}},
         # per timed step: K1 + K4 (one graph); the per-kernel loop replays them
-        # again from graphs of their own; split-K adds its reduce kernel for small M
-        "gpu_launches": (2 + (1 if m <= 512 else 0)) * args.steps,
+        # again from graphs of their own; split-K (small M) reduces inside K4
+        "gpu_launches": 2 * args.steps,
         "launch": "one CUDA graph per step (K1, then K4 as a programmatic dependent launch); "
                   "K1 and K4 also timed apart from their own graphs for the rooflines",
         "clocks": clk.summary(),

@@ -487,7 +487,7 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, AF != F8, BF != F8>::thread
         }
     } else if (L::packed && warp >= 8) {
         // ---------------- int4 -> int8 unpack warps ----------------
-        const int team = (warp - 8) / L::team_warps;
+        const int team = (warp - 8) / (L::team_warps > 0 ? L::team_warps : 1);
         const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
         int stage = 0, us = 0, step = 0;
         uint32_t phase = 0, uphase = 0;
@@ -670,11 +670,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     // Work of this cluster as segments (tile, kb0, kb1, split).
     //  sk == 0: data-parallel, whole tiles round robin (split = -1).
     //  sk >= 2: split-K by sk (small M): cluster cid takes split s = cid % sk of
-    //    tile cid / sk and writes its raw INT32 partial to the full-size plane
-    //    ws[s][M][N]; k_splitk_reduce sums the planes and runs the epilogue.
+    //    tile cid / sk. Split s owns the 32-column chunks c = s, s + sk, ...: it
+    //    writes the chunks it does not own as raw INT32 partials to its workspace
+    //    slot (coalesced [chunk][v][row][4] layout), counts itself in, waits for
+    //    the tile's other splits (all clusters are co-resident: the grid is at
+    //    most one CTA per SM) and sums their partials of its own chunks into its
+    //    accumulator before the epilogue (no second kernel, no full-size planes).
     // Integer partial sums: exact and order-free. Split-K only exists in the
     // NB = 1 instantiation (small M); the 256 x 512 kernel is data-parallel.
     constexpr bool SPLITS = NB == 1;
+    static_assert(!SPLITS || NG == 1, "split-K fix-up barrier counts the 4 epilogue warps");
     auto for_each_seg = [&](auto&& f) {
         if (SPLITS && sk >= 2) {
             if (cid < num_tiles * sk) {
@@ -824,21 +829,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
 #pragma unroll
                     for (int e = 0; e < 32; ++e) r[e] = static_cast<uint32_t>(c + e);
                 }
-                if (plane) {
-                    const int col0 = n_blk * TN + c * 32;
-                    if (row < m && col0 < n) {
-                        int32_t* dst = ws + (static_cast<int64_t>(split) * m + row) * n + col0;
-                        if (col0 + 32 <= n && (n & 3) == 0) {
+                if (plane) {  // chunks owned by another split -> slot (512-byte warp stores)
+                    if (c % sk == split) continue;
+                    int4* slot = reinterpret_cast<int4*>(ws) +
+                                 ((static_cast<int64_t>(tile * 2 + rank) * sk + split) * (TN / 32) + c) *
+                                     8 * BM + ew * 32 + lane;
 #pragma unroll
-                            for (int v = 0; v < 8; ++v)
-                                reinterpret_cast<int4*>(dst)[v] =
-                                    make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-                        } else {
-#pragma unroll
-                            for (int e = 0; e < 32; ++e)
-                                if (col0 + e < n) dst[e] = static_cast<int32_t>(r[e]);
-                        }
-                    }
+                    for (int v = 0; v < 8; ++v)
+                        slot[v * BM] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
                     continue;
                 }
                 const int col0 = n_blk * TN + c * 32;
@@ -888,6 +886,58 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                 }
             }
             }  // sub-tiles
+            if (plane) {
+                // count this split in (release: every writer fences, one thread adds)
+                // and wait until the tile's sk splits all have (acquire)
+                __threadfence();
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                if (ew == 0 && lane == 0) {
+                    int* cnt = reinterpret_cast<int*>(
+                                   ws + static_cast<int64_t>(num_tiles) * 2 * sk * BM * TN) +
+                               tile * 2 + rank;
+                    atomicAdd(cnt, 1);
+                    int v;
+                    do {
+                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+                    } while (v < sk);
+                }
+                asm volatile("bar.sync 1, 128;" ::: "memory");
+                const int rloc = rank * BM + ew * 32 + lane;
+                const int row = m_blk * TM + rloc;
+                const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
+                const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
+                const int4* slots = reinterpret_cast<const int4*>(ws) +
+                                    static_cast<int64_t>(tile * 2 + rank) * sk * (TN / 32) * 8 * BM +
+                                    ew * 32 + lane;
+#pragma unroll 1
+                for (int c = split; c < TN / 32; c += sk) {
+                    uint32_t r[32];
+                    ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+                    ptx::tmem_wait_ld();
+#pragma unroll 1
+                    for (int sp = 0; sp < sk; sp += 2) {  // two partials in flight
+                        const bool u0 = sp != split, u1 = sp + 1 < sk && sp + 1 != split;
+                        const int4* p0 = slots + (static_cast<int64_t>(sp) * (TN / 32) + c) * 8 * BM;
+                        const int4* p1 = p0 + (TN / 32) * 8 * BM;
+                        int4 a0[8], a1[8];
+#pragma unroll
+                        for (int v = 0; v < 8; ++v) {
+                            a0[v] = u0 ? __ldcg(p0 + v * BM) : make_int4(0, 0, 0, 0);
+                            a1[v] = u1 ? __ldcg(p1 + v * BM) : make_int4(0, 0, 0, 0);
+                        }
+#pragma unroll
+                        for (int v = 0; v < 8; ++v) {
+                            r[4 * v] += a0[v].x + a1[v].x, r[4 * v + 1] += a0[v].y + a1[v].y;
+                            r[4 * v + 2] += a0[v].z + a1[v].z, r[4 * v + 3] += a0[v].w + a1[v].w;
+                        }
+                    }
+                    const int col0 = n_blk * TN + c * 32;
+                    if (row < m && col0 < n)
+                        store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
+                                             bias_dt, col0, min(32, n - col0), vec_ok != 0, corr, s32,
+                                             cvt_mode(small_acc, s32));
+                }
+            }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0 && (HELP_ALL || grp == 0))
@@ -1011,7 +1061,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
         run_epilogue(warp - 4, 0);
     } else if (L::packed && warp >= 8 && warp < 8 + L::unpack_warps) {
         // ---------------- int4 -> int8 unpack warps (both CTAs) ----------------
-        const int team = (warp - 8) / L::team_warps;
+        const int team = (warp - 8) / (L::team_warps > 0 ? L::team_warps : 1);
         const int utid = threadIdx.x - 256 - 32 * L::team_warps * team, nut = 32 * L::team_warps;
         int stage = 0, us = 0, step = 0;
         uint32_t phase = 0, uphase = 0;
@@ -1077,26 +1127,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gend));
         g_dbg[blockIdx.x % 296][0] = gstart;
         g_dbg[blockIdx.x % 296][3] = gend;
-    }
-}
-
-// Split-K epilogue: y = epi(sum of the split planes), quantize.cpp:190-198
-// (+ the biased-int4 row-sum correction and the optional bias).
-template <int OUT>
-__global__ void __launch_bounds__(256)
-    k_splitk_reduce(const int32_t* __restrict__ ws, int splits, int m, int n, void* __restrict__ y,
-                    int64_t ldy, const double* __restrict__ scale, const void* __restrict__ bias,
-                    int bias_dt, const int32_t* __restrict__ rowsum) {
-    const double s = OUT == FQG_I32 ? 1.0 : __dmul_rn(scale[0], scale[1]);
-    const int64_t total = static_cast<int64_t>(m) * n;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        int32_t acc = 0;
-        for (int sp = 0; sp < splits; ++sp) acc += __ldcs(ws + sp * total + i);
-        const int row = static_cast<int>(i / n), col = static_cast<int>(i % n);
-        if (rowsum != nullptr) acc -= 8 * rowsum[row];
-        const double b = bias ? load_bias(bias, bias_dt, col) : 0.0;
-        store_one<OUT>(y, static_cast<int64_t>(row) * ldy + col, acc, s, b);
     }
 }
 
@@ -1185,9 +1215,13 @@ void launch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t stream) {
     const int sk = p.splits;  // 0, or >= 2 split-K planes (plan_gemm)
     const int nclusters = p.ctas / 2;
     int32_t* ws = nullptr;
-    if (sk >= 2)
-        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws),
-                                 static_cast<size_t>(sk) * g.m * g.n * 4, stream));
+    if (sk >= 2) {  // per (tile, CTA): sk slots of 128 x tile_n INT32, then the counters
+        const int64_t tiles = ((g.m + L::MBS * 2 * BM - 1) / (L::MBS * 2 * BM)) *
+                              ((g.n + L::NBS * L::BN - 1) / (L::NBS * L::BN));
+        const size_t slot_bytes = static_cast<size_t>(tiles) * 2 * sk * BM * L::NBS * L::BN * 4;
+        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), slot_bytes + tiles * 2 * 4, stream));
+        FQG_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(ws) + slot_bytes, 0, tiles * 2 * 4, stream));
+    }
     CUtensorMap ty;
     std::memset(&ty, 0, sizeof(ty));
     const bool tma_y = epi_block_bytes<OUT>() > 0 && vec && sk < 2 && L::epi_groups == 1;
@@ -1225,14 +1259,6 @@ void launch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t stream) {
         tma_y ? 1 : 0,
         small_acc(g) ? 1 : 0);
     if (le == cudaSuccess) le = cudaGetLastError();
-    if (le == cudaSuccess && sk >= 2) {
-        const int64_t total = g.m * g.n;
-        const int rgrid = static_cast<int>(std::min<int64_t>((total + 255) / 256, 8 * num_sms(dev)));
-        k_splitk_reduce<OUT><<<rgrid, 256, 0, stream>>>(
-            ws, sk, static_cast<int>(g.m), static_cast<int>(g.n), g.y, g.ldy, g.scale, g.bias,
-            g.bias_dtype, BF == FU4 ? g.rowsum : nullptr);
-        le = cudaGetLastError();
-    }
     if (ws) cudaFreeAsync(ws, stream);
     FQG_CUDA(le);
     if (dbg) {

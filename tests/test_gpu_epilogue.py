@@ -22,7 +22,7 @@ PATHS = {  # name: (M, N, K', expected plan {kernel, tile_n, splits>1})
     "pair_small_m_splitk": (100, 2048, 2048, (2, 256, True)),
     "pair_256x256": (1024, 2560, 512, (2, 256, False)),
     "pair_256x512": (2048, 3072, 256, (2, 512, False)),
-    "splitk_reduce": (256, 1024, 2048, (2, 256, True)),
+    "splitk_fixup_ragged": (200, 1000, 2048, (2, 256, True)),
     "pair_512x256_int4_weights": (2048, 3072, 256, (2, 256, False)),  # packed B: 512-row tiles
 }
 PACKED_B = {"pair_512x256_int4_weights"}
