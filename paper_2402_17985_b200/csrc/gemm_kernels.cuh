@@ -539,6 +539,7 @@ __global__ void __launch_bounds__(Layout<BN, STAGES, AF != F8, BF != F8>::thread
 // Developer instrumentation (FQG_GEMM_DEBUG=1): per-CTA cycles spent in each
 // role's barrier waits. Off by default (one predicated branch per wait).
 __device__ unsigned long long g_dbg[296][8];
+__device__ unsigned long long g_dbg3[296][8];  // arrival (ns after start) at the final sync per warp role
 __device__ __align__(16) double g_sink[32 * 32];  // FQG_GEMM_DEBUG bit 16
 __device__ unsigned long long g_dbg2[296][8];  // pair packed path: see launch_pair
 #define FQG_TWAIT2(slot, ...)                                                  \
@@ -659,6 +660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     uint64_t* tfull = uempty + U;            // own: accumulator ready
     uint64_t* tempty = tfull + 2;            // leader: accumulator drained (both CTAs)
     uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+    __shared__ uint32_t s_fixup;  // split-K: the chunks this CTA claimed
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
@@ -672,10 +674,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     //  sk >= 2: split-K by sk (small M): cluster cid takes split s = cid % sk of
     //    tile cid / sk. Split s owns the 32-column chunks c = s, s + sk, ...: it
     //    writes the chunks it does not own as raw INT32 partials to its workspace
-    //    slot (coalesced [chunk][v][row][4] layout), counts itself in, waits for
-    //    the tile's other splits (all clusters are co-resident: the grid is at
-    //    most one CTA per SM) and sums their partials of its own chunks into its
-    //    accumulator before the epilogue (no second kernel, no full-size planes).
+    //    slot (coalesced [chunk][v][row][4] layout), counts itself in and waits
+    //    for the tile's other splits (the grid is at most one CTA per SM, so they
+    //    normally run together), then sums their partials of its own chunks into
+    //    its accumulator before the epilogue. The wait is bounded (~20 us): a
+    //    split whose peers are not resident (SMs held by other work, an SM-
+    //    limited context) writes its own chunks too, marks them orphaned and
+    //    leaves; the split that arrives last finishes orphaned chunks. Nothing
+    //    waits on a CTA that has not arrived. No second kernel, no full planes.
     // Integer partial sums: exact and order-free. Split-K only exists in the
     // NB = 1 instantiation (small M); the 256 x 512 kernel is data-parallel.
     constexpr bool SPLITS = NB == 1;
@@ -887,30 +893,49 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             }
             }  // sub-tiles
             if (plane) {
-                // count this split in (release: every writer fences, one thread adds)
-                // and wait until the tile's sk splits all have (acquire)
+                // count this split in (release: every writer fences, one thread adds).
+                // One word per (tile, CTA): arrivals in bits 0-7, chunks orphaned by a
+                // split that stopped waiting in bits 8 + c.
                 __threadfence();
                 asm volatile("bar.sync 1, 128;" ::: "memory");
+                unsigned int* const ctl = reinterpret_cast<unsigned int*>(
+                                              ws + static_cast<int64_t>(num_tiles) * 2 * sk * BM * TN) +
+                                          (tile * 2 + rank);
                 if (ew == 0 && lane == 0) {
-                    int* cnt = reinterpret_cast<int*>(
-                                   ws + static_cast<int64_t>(num_tiles) * 2 * sk * BM * TN) +
-                               tile * 2 + rank;
-                    atomicAdd(cnt, 1);
-                    int v;
-                    do {
-                        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-                    } while (v < sk);
+                    const unsigned int old = atomicAdd(ctl, 1u);
+                    const bool last = (old & 0xFFu) == static_cast<unsigned int>(sk - 1);
+                    bool all_in = last;
+                    // (debug bit 128: never wait, every split but the last orphans)
+                    if (!last && !(dbg & 128)) {  // wait for the other splits, at most ~20 us
+                        unsigned long long t0, t1;
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                        for (;;) {
+                            unsigned int v;
+                            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(ctl) : "memory");
+                            if ((v & 0xFFu) >= static_cast<unsigned int>(sk)) {
+                                all_in = true;
+                                break;
+                            }
+                            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                            if (t1 - t0 > 20000ull) break;
+                        }
+                    }
+                    if (all_in) __threadfence();  // acquire side for the slot reads below
+                    // bit 0: reduce own chunks; bit 1: wrote own chunks, decide after;
+                    // bits 8..: orphaned chunks this (last) split must also reduce
+                    s_fixup = (all_in ? 1u : 2u) | (last ? (old & 0xFF00u) : 0u);
                 }
                 asm volatile("bar.sync 1, 128;" ::: "memory");
+                uint32_t mode = s_fixup;
                 const int rloc = rank * BM + ew * 32 + lane;
                 const int row = m_blk * TM + rloc;
                 const int32_t corr = (BF == FU4 && row < m) ? 8 * rowsum[row] : 0;
                 const uint32_t t_row = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN;
-                const int4* slots = reinterpret_cast<const int4*>(ws) +
-                                    static_cast<int64_t>(tile * 2 + rank) * sk * (TN / 32) * 8 * BM +
-                                    ew * 32 + lane;
-#pragma unroll 1
-                for (int c = split; c < TN / 32; c += sk) {
+                const int4* const slots = reinterpret_cast<const int4*>(ws) +
+                                          static_cast<int64_t>(tile * 2 + rank) * sk * (TN / 32) * 8 * BM +
+                                          ew * 32 + lane;
+                // accumulator chunk c plus the other splits' partials -> y
+                auto reduce_chunk = [&](int c) {
                     uint32_t r[32];
                     ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
                     ptx::tmem_wait_ld();
@@ -936,7 +961,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                         store_row_chunk<OUT>(y, static_cast<int64_t>(row) * ldy + col0, r, s, bias,
                                              bias_dt, col0, min(32, n - col0), vec_ok != 0, corr, s32,
                                              cvt_mode(small_acc, s32));
+                };
+                if (mode & 2u) {  // stopped waiting: own chunks -> slot as well, then orphan them
+#pragma unroll 1
+                    for (int c = split; c < TN / 32; c += sk) {
+                        uint32_t r[32];
+                        ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
+                        ptx::tmem_wait_ld();
+                        int4* slot = reinterpret_cast<int4*>(ws) +
+                                     ((static_cast<int64_t>(tile * 2 + rank) * sk + split) * (TN / 32) + c) *
+                                         8 * BM + ew * 32 + lane;
+#pragma unroll
+                        for (int v = 0; v < 8; ++v)
+                            slot[v * BM] = make_int4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+                    }
+                    __threadfence();
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    if (ew == 0 && lane == 0) {
+                        unsigned int own = 0;
+                        for (int c = split; c < TN / 32; c += sk) own |= 1u << (8 + c);
+                        // if the last split has arrived meanwhile it will not look at
+                        // these bits: every partial is in, so reduce them here
+                        const unsigned int old = atomicOr(ctl, own);
+                        const bool done_in = (old & 0xFFu) >= static_cast<unsigned int>(sk);
+                        if (done_in) __threadfence();
+                        s_fixup = done_in ? 1u : 0u;
+                    }
+                    asm volatile("bar.sync 1, 128;" ::: "memory");
+                    mode = s_fixup;
                 }
+                if (mode & 1u) {
+#pragma unroll 1
+                    for (int c = split; c < TN / 32; c += sk) reduce_chunk(c);
+                }
+#pragma unroll 1
+                for (int c = 0; c < TN / 32; ++c)  // orphans seen at the last arrival
+                    if ((mode >> (8 + c)) & 1u) reduce_chunk(c);
             }
             ptx::tc_fence_before();
             __syncwarp();
@@ -1115,8 +1175,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
     } else if (NG > 1 && warp >= 8) {  // spare warps: epilogue groups only
         run_epilogue(warp & 3, 1 + (warp - 8) / 4);
     }
+    if (dbg && lane == 0) {
+        unsigned long long ga;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ga));
+        const int role = warp < 4 ? warp : (warp < 8 ? 4 : (warp < 8 + L::unpack_warps ? 5 : 6));
+        atomicMax(&g_dbg3[blockIdx.x % 296][role], ga - gstart);
+    }
     ptx::tc_fence_before();
     ptx::cluster_sync();
+    if (dbg && threadIdx.x == 32) {
+        unsigned long long gs;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gs));
+        g_dbg3[blockIdx.x % 296][7] = gs - gstart;
+    }
     if (warp == 1) {
         __syncwarp();
         ptx::tc_fence_after();
@@ -1210,6 +1281,7 @@ void launch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t stream) {
     if (dbg) {
         static unsigned long long zeros[296][8] = {};
         FQG_CUDA(cudaMemcpyToSymbol(g_dbg, zeros, sizeof(zeros)));
+        FQG_CUDA(cudaMemcpyToSymbol(g_dbg3, zeros, sizeof(zeros)));
         FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
     }
     const int sk = p.splits;  // 0, or >= 2 split-K planes (plan_gemm)
@@ -1219,8 +1291,10 @@ void launch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t stream) {
         const int64_t tiles = ((g.m + L::MBS * 2 * BM - 1) / (L::MBS * 2 * BM)) *
                               ((g.n + L::NBS * L::BN - 1) / (L::NBS * L::BN));
         const size_t slot_bytes = static_cast<size_t>(tiles) * 2 * sk * BM * L::NBS * L::BN * 4;
-        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), slot_bytes + tiles * 2 * 4, stream));
-        FQG_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(ws) + slot_bytes, 0, tiles * 2 * 4, stream));
+        static_assert(NB != 1 || L::NBS * L::BN / 32 <= 8, "split-K control word: 8 chunk bits");
+        const size_t ctl_bytes = static_cast<size_t>(tiles) * 2 * 4;
+        FQG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&ws), slot_bytes + ctl_bytes, stream));
+        FQG_CUDA(cudaMemsetAsync(reinterpret_cast<uint8_t*>(ws) + slot_bytes, 0, ctl_bytes, stream));
     }
     CUtensorMap ty;
     std::memset(&ty, 0, sizeof(ty));
@@ -1305,6 +1379,22 @@ void launch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t stream) {
             for (int i = 0; i < 8; ++i) a2[i] += static_cast<double>(h2[c][i]) / nc;
         std::fprintf(stderr, "[fqg gemm pair] epilogue: accumulator ready at %.1f us, done at %.1f us (avg per CTA, summed over its tiles)\n",
                      a2[6] * 1e-3, a2[7] * 1e-3);
+        {
+            unsigned long long h3[296][8];
+            FQG_CUDA(cudaMemcpyFromSymbol(h3, g_dbg3, sizeof(h3)));
+            double a3[8] = {0}, m3[8] = {0};
+            for (int c = 0; c < nc; ++c)
+                for (int i = 0; i < 8; ++i) {
+                    a3[i] += static_cast<double>(h3[c][i]) / nc;
+                    m3[i] = std::max(m3[i], static_cast<double>(h3[c][i]));
+                }
+            std::fprintf(stderr,
+                         "[fqg gemm pair] final-sync arrival avg/max us: producer %.1f/%.1f mma %.1f/%.1f "
+                         "w2 %.1f w3 %.1f epi %.1f/%.1f unpack %.1f/%.1f spare %.1f/%.1f | past sync %.1f/%.1f\n",
+                         a3[0] * 1e-3, m3[0] * 1e-3, a3[1] * 1e-3, m3[1] * 1e-3, a3[2] * 1e-3,
+                         a3[3] * 1e-3, a3[4] * 1e-3, m3[4] * 1e-3, a3[5] * 1e-3, m3[5] * 1e-3,
+                         a3[6] * 1e-3, m3[6] * 1e-3, a3[7] * 1e-3, m3[7] * 1e-3);
+        }
         std::fprintf(stderr,
                      "[fqg gemm pair] per CTA: mma wait ufull %.0f, wait full_mma %.0f | unpack "
                      "(thread 0): wait full_unp %.0f, wait uempty %.0f, work %.0f cyc over %.0f "

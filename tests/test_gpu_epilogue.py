@@ -8,9 +8,14 @@ reference output exactly.
 
 Paths (asserted with fqg_gemm_plan, so a dispatch change cannot silently skip
 one): the 1-CTA 128 x N kernel, the CTA-pair kernel with 256 x 256 tiles, the
-pair kernel with 256 x 512 tiles, and the split-K planes + reduce kernel.
+pair kernel with 256 x 512 tiles, the 512 x 256 tiles of packed int4 weights,
+and split-K with its in-kernel fix-up (including the orphaned-chunk path a split
+takes when its peers are not resident, forced by debug bit 128).
 """
 import ctypes as C
+import os
+import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -105,6 +110,19 @@ def test_epilogue_out_and_bias(fq, path):
             assert bad.size == 0, (f"{path} out={out} bias={bias_dt}: {len(bad)} mismatches, "
                                    f"e.g. {tuple(bad[0])}: {got[tuple(bad[0])]} vs "
                                    f"{want[tuple(bad[0])]}")
+
+
+@pytest.mark.skipif(os.environ.get("FQG_GEMM_DEBUG") == "128", reason="already the child run")
+def test_splitk_orphaned_chunks():
+    """Split-K with no waiting at all: every split but the last writes its own
+    chunks too and leaves; the last split reduces them. Same bits as the normal
+    path (run in a child process: the debug bits are read once per process)."""
+    env = dict(os.environ, FQG_GEMM_DEBUG="128")
+    r = subprocess.run([sys.executable, "-m", "pytest", __file__, "-q", "-m", "gpu", "-x",
+                        "-k", "splitk and not orphaned", "-p", "no:cacheprovider"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
+    assert " passed" in r.stdout, r.stdout[-2000:]
 
 
 @pytest.mark.parametrize("out", ["f16", "bf16", "f32"])
