@@ -246,20 +246,32 @@ class LayerBench:
             torch.cuda.current_stream().cuda_stream))
 
     def capture(self, warmup):
+        """Graphs: step (K1, K4), K1 alone, K4 alone. Each carries external event
+        record nodes around its kernels, so the device time of the kernels is read
+        without the graph's launch latency (a model replays all its layers from
+        one graph); events outside the graph give the launch-inclusive time."""
         import torch
 
         for _ in range(warmup):
             self.k1()
             self.k4()
         torch.cuda.synchronize()
+        E = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731
+        self.ev_in = {name: (E(), E()) for name in ("step", "k1", "k4")}
         g1, g4, gs = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(g1):
+            self.ev_in["k1"][0].record()
             self.k1()
+            self.ev_in["k1"][1].record()
         with torch.cuda.graph(g4):
+            self.ev_in["k4"][0].record()
             self.k4()
+            self.ev_in["k4"][1].record()
         with torch.cuda.graph(gs):
+            self.ev_in["step"][0].record()
             self.k1()
             self.k4()
+            self.ev_in["step"][1].record()
         self.k1_runs -= 3  # the captures did not execute
         for _ in range(2):
             g1.replay()
@@ -270,11 +282,20 @@ class LayerBench:
         self.graphs = (g1, g4, gs)
 
     def time(self, steps, after_step=None):
-        """(t_step, t_k1, t_k4, t_after) in ms, means over `steps` flushed replays."""
+        """Means over `steps` flushed replays, in ms: (t_step, t_k1, t_k4, t_after,
+        t_step_launch). t_step / t_k1 / t_k4 are device times between the event
+        nodes inside the graphs; t_step_launch brackets the graph launch itself."""
         import torch
 
         g1, g4, gs = self.graphs
         E = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+        acc = {"step": [], "k1": [], "k4": [], "after": [], "launch": []}
+
+        def inner(name):
+            a, b = self.ev_in[name]
+            return a.elapsed_time(b)
+
+        # launch-inclusive pass: events around the replays, no host syncs in between
         ev = [(E(), E(), E()) for _ in range(steps)]
         for i in range(steps):
             self.flush.fill_(i & 255)
@@ -284,21 +305,27 @@ class LayerBench:
             if after_step is not None:
                 after_step()
             ev[i][2].record()
-        sp = [(E(), E(), E()) for _ in range(steps)]
+        torch.cuda.synchronize()
+        acc["launch"] = [a.elapsed_time(b) for a, b, _ in ev]
+        acc["after"] = [b.elapsed_time(c) for _, b, c in ev]
+        # device pass: the in-graph event nodes (read after each replay)
         for i in range(steps):
             self.flush.fill_(i & 255)
-            sp[i][0].record()
+            gs.replay()
+            torch.cuda.synchronize()  # the in-graph events are re-recorded by every replay
+            acc["step"].append(inner("step"))
+        for i in range(steps):
+            self.flush.fill_(i & 255)
             g1.replay()
-            sp[i][1].record()
-            g4.replay()
-            sp[i][2].record()
-        torch.cuda.synchronize()
-        self.k1_runs += 2 * steps
+            torch.cuda.synchronize()
+            acc["k1"].append(inner("k1"))
+            g4.replay()  # (K1's operand is in L2, as inside the step)
+            torch.cuda.synchronize()
+            acc["k4"].append(inner("k4"))
+        self.k1_runs += 3 * steps
         mean = lambda v: float(sum(v) / len(v))  # noqa: E731
-        return (mean([a.elapsed_time(b) for a, b, _ in ev]),
-                mean([a.elapsed_time(b) for a, b, _ in sp]),
-                mean([b.elapsed_time(c) for _, b, c in sp]),
-                mean([b.elapsed_time(c) for _, b, c in ev]))
+        return (mean(acc["step"]), mean(acc["k1"]), mean(acc["k4"]), mean(acc["after"]),
+                mean(acc["launch"]))
 
 
 def layer_result(fq, cfg, k, n, m, bits, x, steps, warmup, i8_peak, n_begin=0, n_cols=None,
@@ -312,12 +339,13 @@ def layer_result(fq, cfg, k, n, m, bits, x, steps, warmup, i8_peak, n_begin=0, n
     xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
     lb = LayerBench(fq, layer, xt, flush=flush)
     lb.capture(warmup)
-    t_step, t_k1, t_k4, _ = lb.time(steps)
+    t_step, t_k1, t_k4, _, t_launch = lb.time(steps)
     ops = 2.0 * m * n_cols * layer.kp
     res = {"K": k, "N": n_cols, "M": m, "bits": bits, "Kp": layer.kp,
            "value": ops / (t_step * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": t_step,
            "tokens_per_s": m / (t_step * 1e-3),
            "breakdown_ms": {"flatten_quant_K1": t_k1, "gemm_K4": t_k4, "K1_K4_graph": t_step},
+           "ms_per_step_with_launch": t_launch,
            "roofline_frac_K4": ops / (t_k4 * 1e-3) / 1e12 / i8_peak}
     del lb, layer, xt
     torch.cuda.empty_cache()
@@ -469,7 +497,8 @@ def main():
     with Clocks(local_rank) as clk:
         torch.cuda.synchronize()
         barrier()
-        t_k1k4, t_k1, t_k4, t_ag = lb.time(args.steps, after_step=gather if world > 1 else None)
+        t_k1k4, t_k1, t_k4, t_ag, t_launch = lb.time(args.steps,
+                                                     after_step=gather if world > 1 else None)
         torch.cuda.synchronize()
         barrier()
     t_step = t_k1k4 + (t_ag if world > 1 else 0.0)
@@ -527,6 +556,9 @@ def main():
         "metric": METRIC, "value": tops, "unit": "TOPS",
         "tokens_per_s": m / (t_step * 1e-3),
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step,
+        "timing": "device time between event-record nodes captured inside the step's CUDA graph "
+                  "(K1 -> K4 [-> all-gather]); ms_per_step_with_launch adds the graph launch",
+        "ms_per_step_with_launch": t_launch + (t_ag if world > 1 else 0.0),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "int8 MMA / int32 accumulate (4-bit values)" if bits == 4 else
                  "int8 MMA / int32 accumulate",

@@ -15,4 +15,6 @@ timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/b
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-subresults --e2e-steps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_i8_pair -s 3 -c 1 -o gpurun_out/prof_gemm python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-subresults --e2e-steps 1 > /dev/null 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_flatten16 -s 3 -c 1 -o gpurun_out/prof_k1 python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-subresults --e2e-steps 1 > /dev/null 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_gemm_i8_pair -s 3 -c 1 -o gpurun_out/prof_gemm_m256 python bench.py --config w8a8_4096_m256 --steps 2 --warmup 3 --no-cpu-baseline --no-subresults --e2e-steps 1 > /dev/null 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/launches_m256.csv python bench.py --config w8a8_4096_m256 --steps 3 --warmup 3 --no-cpu-baseline --no-subresults --e2e-steps 1 > /dev/null 2>&1
 ls -la gpurun_out
