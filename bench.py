@@ -52,6 +52,18 @@ SWEEP_M = [1, 16, 128, 256, 512, 1024, 2048, 4096, 8192]  # configs[4]
 SPEC_INT8_TOPS = 4500.0
 
 
+def gemm_label(fq, m, n, kp, a_fmt, b_fmt):
+    """K4's launch plan for this shape, as fqg_gemm_plan reports it."""
+    from paper_2402_17985_b200 import _lib
+
+    info = _lib.GemmPlan()
+    fq.check(fq.lib().fqg_gemm_plan(m, n, kp, a_fmt, b_fmt, _lib.F16, ctypes.byref(info)))
+    name = ("k_gemm_i8_pair (tcgen05.mma.cta_group::2.kind::i8" if info.kernel == 2 else
+            "k_gemm_i8 (tcgen05.mma.cta_group::1.kind::i8")
+    split = f", split-K x{info.splits}" if info.splits > 1 else ""
+    return f"{name}, {info.tile_m}x{info.tile_n} tiles{split}, {info.ctas} CTAs)"
+
+
 def peaks():
     """(HBM GB/s, bf16 TFLOP/s, source, INT8 MMA TOPS, source)."""
     try:
@@ -576,7 +588,7 @@ def main():
         "saturation_events_per_step": sat_per_step,  # counted by K1 in every timed step
         "roofline": {"bound": "tensor", "achieved": gemm_tops, "peak": int8_peak,
                      "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
-                     "kernel": "k_gemm_i8_pair (tcgen05.mma.cta_group::2.kind::i8, 256x512 tiles)",
+                     "kernel": gemm_label(fq, m, b1 - b0, kp, a_fmt, b_fmt),
                      "peak_basis": f"tcgen05 kind::i8 MMA peak, {i8_src}; frac vs spec 4.5 "
                                    f"POPS: {gemm_tops / SPEC_INT8_TOPS:.3f}; vs 2 x bf16 "
                                    f"measured ({peak_src}): {gemm_tops / (2 * bf16_tf):.3f}",
