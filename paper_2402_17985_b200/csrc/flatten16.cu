@@ -167,6 +167,7 @@ __device__ __forceinline__ uint32_t pack_i4_word(uint32_t lo, uint32_t hi) {
 // The per-row operand sums (biased-int4 GEMM epilogue) are accumulated on the
 // way (dp4a of the tier-1 words and copy words, corrections and extension
 // pieces of the splits) instead of by a re-read of the rows.
+constexpr int kThreads = 256;
 constexpr int kMaxHot = 128;  // hot channels (layer.cu caps the list)
 constexpr int kListCap = 1024;  // compacted tier-2 elements per block
 
@@ -204,9 +205,8 @@ __device__ __forceinline__ void fill_pieces(int8_t* d, int last, int ce, int fv,
     if (ce <= last) d[ce - 1] = static_cast<int8_t>(qe);
 }
 
-template <bool F16, bool PACK4, int R, int T>
-__global__ void __launch_bounds__(T, (R >= 8 ? 2 : 4) * (256 / T)) k_flatten16(const __grid_constant__ K16Params p) {
-    constexpr int kThreads = T;
+template <bool F16, bool PACK4, int R>
+__global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __grid_constant__ K16Params p) {
     ptx::griddep_launch_dependents();  // K4 may start its prologue (it waits for our stores)
     extern __shared__ __align__(16) uint8_t sm[];
     const int tid = threadIdx.x;
@@ -435,7 +435,7 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     };
     while (rb > 1 && smem_of(rb) > 200 * 1024) rb >>= 1;
     const size_t smem = smem_of(rb);
-    if (smem > 200 * 1024) return false;
+    if (smem > 220 * 1024) return false;
     K16Params p{};
     p.x = a.x;
     p.ldx = a.ldx;
@@ -473,34 +473,26 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     p.sat = a.sat;
     p.rowsum = a.rowsum;
     const bool f16 = a.x_dtype == FQG_F16;
-    static const int threads_env = [] {  // tuning override: FQG_K1_THREADS = 128 or 256
-        const char* e = std::getenv("FQG_K1_THREADS");
-        return e ? std::atoi(e) : 0;
-    }();
+    const unsigned grid = static_cast<unsigned>((a.m + rb - 1) / rb);
     auto go = [&](auto rc) {
         constexpr int R = decltype(rc)::value;
-        auto run = [&](auto tc) {
-            constexpr int T = decltype(tc)::value;
-            const unsigned grid = static_cast<unsigned>((a.m + rb - 1) / rb);
-            if (f16 && a.pack4) {
-                ensure_smem_attr<k_flatten16<true, true, R, T>>(200 * 1024);
-                k_flatten16<true, true, R, T><<<grid, T, smem, st>>>(p);
-            } else if (f16) {
-                ensure_smem_attr<k_flatten16<true, false, R, T>>(200 * 1024);
-                k_flatten16<true, false, R, T><<<grid, T, smem, st>>>(p);
-            } else if (a.pack4) {
-                ensure_smem_attr<k_flatten16<false, true, R, T>>(200 * 1024);
-                k_flatten16<false, true, R, T><<<grid, T, smem, st>>>(p);
-            } else {
-                ensure_smem_attr<k_flatten16<false, false, R, T>>(200 * 1024);
-                k_flatten16<false, false, R, T><<<grid, T, smem, st>>>(p);
-            }
+        auto run = [&](auto kern) {
+            kern<<<grid, kThreads, smem, st>>>(p);
             FQG_CUDA(cudaGetLastError());
         };
-        if (threads_env == 128)
-            run(std::integral_constant<int, 128>{});
-        else
-            run(std::integral_constant<int, 256>{});
+        if (f16 && a.pack4) {
+            ensure_smem_attr<k_flatten16<true, true, R>>(220 * 1024);
+            run(k_flatten16<true, true, R>);
+        } else if (f16) {
+            ensure_smem_attr<k_flatten16<true, false, R>>(220 * 1024);
+            run(k_flatten16<true, false, R>);
+        } else if (a.pack4) {
+            ensure_smem_attr<k_flatten16<false, true, R>>(220 * 1024);
+            run(k_flatten16<false, true, R>);
+        } else {
+            ensure_smem_attr<k_flatten16<false, false, R>>(220 * 1024);
+            run(k_flatten16<false, false, R>);
+        }
     };
     switch (rb) {
         case 8: go(std::integral_constant<int, 8>{}); break;
