@@ -271,14 +271,16 @@ std::vector<Tensor> read_fqta(const std::string& path) {
         x.cols = static_cast<int64_t>(cols);
         const size_t n = static_cast<size_t>(rows * cols);
         if (dtype == 0) {
+            const char* src = take(n * 8);  // bounds-checked before the allocation
             x.f.resize(n);
-            std::memcpy(x.f.data(), take(n * 8), n * 8);
+            std::memcpy(x.f.data(), src, n * 8);
             for (double v : x.f)
                 if (!std::isfinite(v)) throw Error(FQG_ERR_RUNTIME, "non-finite value in tensor: " + x.name);
         } else {
             x.is_f64 = false;
+            const char* src = take(n * 4);
             x.i.resize(n);
-            std::memcpy(x.i.data(), take(n * 4), n * 4);
+            std::memcpy(x.i.data(), src, n * 4);
         }
         out.push_back(std::move(x));
     }
