@@ -39,6 +39,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <vector>
 #include <type_traits>
 #include <cstdio>
 #include <cstdlib>
@@ -189,6 +190,7 @@ struct K16Params {
     int64_t ldq;
     unsigned long long* sat;
     int32_t* rowsum;
+    long long* dbg;        // FQG_K1_DEBUG: per block {start, zero, tier1, splits, copies, pack, end}
 };
 
 // Extension pieces 1 .. last of one element into d[0 .. last): full pieces
@@ -210,6 +212,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
     ptx::griddep_launch_dependents();  // K4 may start its prologue (it waits for our stores)
     extern __shared__ __align__(16) uint8_t sm[];
     const int tid = threadIdx.x;
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL] = clock64();
     const int k = p.k, kp = p.kp, c1 = p.c1, ldf = p.ldf;
     const int ngrp = k >> 3;  // channel groups of 8
     const int row0 = blockIdx.x * R;
@@ -234,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         }
     }
     __syncthreads();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 1] = clock64();
 
     const bool want_rs = p.rowsum != nullptr;
     int rs[R];
@@ -321,6 +325,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         }
     }
     __syncthreads();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 2] = clock64();
 
     // ---- 2. exact splits: hot channels on every row, then the queued elements ----
     const int nhot_items = nrow * p.nhot;
@@ -342,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         for (int rr = 0; rr < R; ++rr) rs[rr] += rr == r ? d : 0;
     }
     __syncthreads();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 3] = clock64();
 
     // ---- 3. plan_w copies [C1, K') ----
     for (int u = tid; u < ((kp - c1) >> 2); u += kThreads) {
@@ -366,6 +372,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         }
     }
     __syncthreads();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 4] = clock64();
 
     // ---- 4. int4 packing in place, then one bulk copy per row ----
     if constexpr (PACK4) {  // byte i = q[i] & 15 | q[16 + i] << 4 per group of 32
@@ -390,6 +397,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
     }
     ptx::fence_proxy_async_smem();  // generic-proxy SMEM writes -> visible to the bulk copies
     __syncthreads();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 5] = clock64();
     if (tid < nrow) {
         ptx::bulk_store(p.q + static_cast<int64_t>(row0 + tid) * p.ldq, rows + tid * ldf,
                         PACK4 ? static_cast<uint32_t>(kp >> 1) : static_cast<uint32_t>(kp));
@@ -401,6 +409,13 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         if ((tid & 31) == 0 && sat) atomicAdd(p.sat, sat);
     }
     if (tid < nrow) ptx::bulk_wait_all();
+    if (p.dbg && tid == 0) {
+        long long* d = p.dbg + static_cast<int64_t>(blockIdx.x) * 8;
+        d[6] = clock64();
+        unsigned int smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        d[7] = smid;
+    }
 }
 
 }  // namespace
@@ -472,6 +487,13 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     p.ldq = a.ldq;
     p.sat = a.sat;
     p.rowsum = a.rowsum;
+    static const bool k1_dbg = std::getenv("FQG_K1_DEBUG") != nullptr;
+    long long* dbg_buf = nullptr;
+    const int64_t nblk_dbg = (a.m + rb - 1) / rb;
+    if (k1_dbg) {
+        FQG_CUDA(cudaMalloc(&dbg_buf, nblk_dbg * 8 * sizeof(long long)));
+        p.dbg = dbg_buf;
+    }
     const bool f16 = a.x_dtype == FQG_F16;
     const unsigned grid = static_cast<unsigned>((a.m + rb - 1) / rb);
     auto go = [&](auto rc) {
@@ -499,6 +521,17 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
         case 4: go(std::integral_constant<int, 4>{}); break;
         case 2: go(std::integral_constant<int, 2>{}); break;
         default: go(std::integral_constant<int, 1>{}); break;
+    }
+    if (k1_dbg) {  // developer instrumentation: mean cycles per phase, per-SM spread
+        std::vector<long long> h(nblk_dbg * 8);
+        FQG_CUDA(cudaStreamSynchronize(st));
+        FQG_CUDA(cudaMemcpy(h.data(), dbg_buf, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+        cudaFree(dbg_buf);
+        double ph[6] = {0};
+        for (int64_t b = 0; b < nblk_dbg; ++b)
+            for (int i = 0; i < 6; ++i) ph[i] += static_cast<double>(h[b * 8 + i + 1] - h[b * 8 + i]) / nblk_dbg;
+        std::fprintf(stderr, "[fqg k1] R=%d blocks=%lld mean cycles: zero %.0f tier1 %.0f splits %.0f copies %.0f pack %.0f store %.0f\n",
+                     rb, static_cast<long long>(nblk_dbg), ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
     }
     return true;
 }
