@@ -187,8 +187,10 @@ int fqg_gemm(const void* a_dev, int a_fmt, int64_t lda, const void* b_dev, int b
 
 /* The launch fqg_gemm (and a layer's GEMM) makes for a shape, on the current
  * device; host-only query for tests and tooling. kernel 1: 1-CTA 128 x tile_n
- * tiles; kernel 2: CTA pair (cta_group::2) 256 x tile_n tiles; splits >= 2:
- * split-K into INT32 planes plus a reduce/epilogue kernel; ctas: grid size. */
+ * tiles; kernel 2: CTA pair (cta_group::2) tile_m x tile_n tiles (tile_m 512:
+ * two A sub-tiles); kernel 3: decode-size M (<= 4 rows) on CUDA cores, tile_n
+ * columns per warp; splits >= 2: split-K with the fix-up inside the kernel;
+ * ctas: grid size. */
 typedef struct fqg_gemm_plan_info {
     int kernel, tile_m, tile_n, splits, ctas;
 } fqg_gemm_plan_info;

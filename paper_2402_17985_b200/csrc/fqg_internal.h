@@ -104,9 +104,10 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream);
 
 // The launch gemm_i8 makes for a shape (fqg_gemm_plan exposes it).
 struct GemmPlan {
-    int kernel = 0;           // 1: 1-CTA 128 x tile_n tiles; 2: CTA pair 256 x tile_n
+    int kernel = 0;           // 1: 1-CTA 128 x tile_n tiles; 2: CTA pair 256 x tile_n;
+                              // 3: decode-size M on CUDA cores (gemv.cu)
     int tile_m = 0, tile_n = 0;
-    int splits = 0;           // >= 2: split-K planes + k_splitk_reduce
+    int splits = 0;           // >= 2: split-K with the in-kernel fix-up
     int ctas = 0;             // grid size
 };
 GemmPlan plan_gemm(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int variant, int sms);

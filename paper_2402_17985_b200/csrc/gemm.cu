@@ -12,6 +12,7 @@ void gemm_pair_FS4_FS4(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
 void gemm_pair_FS4_FU4(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
 void gemm_one_F8(const GemmArgs& g, int bn, cudaStream_t s);
 void gemm_one_FS4(const GemmArgs& g, int bn, cudaStream_t s);
+void gemv_i8(const GemmArgs& g, const GemmPlan& p, cudaStream_t s);
 
 namespace {
 void dispatch_pair_fmt(const GemmArgs& g, const GemmPlan& p, cudaStream_t s) {
@@ -57,7 +58,9 @@ void gemm_i8(const GemmArgs& g, cudaStream_t stream) {
     int dev = 0;
     FQG_CUDA(cudaGetDevice(&dev));
     const GemmPlan p = plan_gemm(g.m, g.n, g.kp, g.a_fmt, g.b_fmt, g.variant, num_sms(dev));
-    if (p.kernel == 2)
+    if (p.kernel == 3)
+        gemv_i8(g, p, stream);
+    else if (p.kernel == 2)
         dispatch_pair_fmt(g, p, stream);
     else if (kfmt(g.a_fmt) == F8)
         gemm_one_F8(g, p.tile_n, stream);
@@ -83,6 +86,15 @@ GemmPlan plan_gemm(int64_t m, int64_t n, int64_t kp, int a_fmt, int b_fmt, int v
     // weights as the MMA's A operand in TMEM) measured 79-87 us and was removed.
     // The pair kernel also for small M: its split-K spreads the weight stream over
     // the CTA pairs (M = 1 at 8192^2: 61 us on 32 single CTAs before).
+    // Decode-size M (1-2 rows, int8 operands): the weight stream on CUDA cores (gemv.cu).
+    if ((v == 0 || v == 3) && m <= 2 && a_fmt == FQG_I8 && b_fmt == FQG_I8) {
+        p.kernel = 3;
+        p.tile_m = 2;
+        p.tile_n = 4;  // output columns per warp pass
+        const int64_t groups = (n + 3) / 4;  // 4-column groups, spread over the CTAs
+        p.ctas = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(groups, 4 * sms)));
+        return p;
+    }
     if (v == 0) v = (n > 128 && a_fmt == FQG_I8) ? 2 : 1;
     const int64_t num_kb = (kp + BK - 1) / BK;
     if (v == 2) {

@@ -9,7 +9,7 @@ reference output exactly.
 Paths (asserted with fqg_gemm_plan, so a dispatch change cannot silently skip
 one): the 1-CTA 128 x N kernel, the CTA-pair kernel with 256 x 256 tiles, the
 pair kernel with 256 x 512 tiles, the 512 x 256 tiles of packed int4 weights,
-and split-K with its in-kernel fix-up (including the orphaned-chunk path a split
+the CUDA-core path for decode-size M (1-2 rows, int8 weights), and split-K with its in-kernel fix-up (including the orphaned-chunk path a split
 takes when its peers are not resident, forced by debug bit 128).
 """
 import ctypes as C
@@ -29,6 +29,8 @@ PATHS = {  # name: (M, N, K', expected plan {kernel, tile_n, splits>1})
     "pair_256x512": (2048, 3072, 256, (2, 512, False)),
     "splitk_fixup_ragged": (200, 1000, 2048, (2, 256, True)),
     "pair_512x256_int4_weights": (2048, 3072, 256, (2, 256, False)),  # packed B: 512-row tiles
+    "gemv_decode": (2, 1000, 2048, (3, None, False)),  # M <= 2: CUDA-core weight stream
+    "gemv_decode_one_row": (1, 4100, 1024, (3, None, False)),
 }
 PACKED_B = {"pair_512x256_int4_weights"}
 OUTS = ["f16", "bf16", "f32", "f64"]
@@ -87,7 +89,7 @@ def test_epilogue_out_and_bias(fq, path):
     for out in OUTS:
         p = plan(fq, m, n, kp, _lib.I8, b_code, code[out])
         assert p.kernel == kern, (path, out, p.kernel)
-        if packed:
+        if packed and kern == 2:
             assert p.tile_m == 512, (path, out, p.tile_m)
         if tile_n is not None:
             assert p.tile_n == tile_n, (path, out, p.tile_n)
@@ -123,6 +125,29 @@ def test_splitk_orphaned_chunks():
                        env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert " passed" in r.stdout, r.stdout[-2000:]
+
+
+@pytest.mark.parametrize("m", [1, 2, 4])
+def test_layer_decode_rows_int4_weights(port, fq, m):
+    """Decode-size M through the layer with biased int4 weights (tensor-core path)."""
+    import torch
+
+    from conftest import bf16_round
+
+    k, n = 1024, 1000
+    w, calib, x = fq.synthetic_layer(5, test_rows=m, in_channels=k, out_channels=n, rows=32,
+                                     samples=4)
+    L = port.quantize_layer(w, calib, 4)
+    x = bf16_round(x)
+    px = fq.FlattenPlan.from_extensions(L.t_x, L.e_x, L.block)
+    pw = fq.FlattenPlan.from_extensions(L.t_w, L.e_w, L.block)
+    cfg = fq.LayerQuantConfig(bits=4, smooth_scales=L.s, plan_x=px, plan_w=pw,
+                              act_scale=L.act_scale, weight_q=L.wq, w_scale=L.s_w)
+    layer = fq.Layer(cfg, a_format=fq.I8, b_format=fq.I4)
+    y_ref, _ = port.run_layer(L, x)
+    xt = torch.from_numpy(x).to(torch.bfloat16).cuda()
+    y = layer.forward(xt, out_dtype=torch.float64).cpu().numpy()
+    assert np.array_equal(y, y_ref)
 
 
 @pytest.mark.parametrize("out", ["f16", "bf16", "f32"])
