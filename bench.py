@@ -406,7 +406,53 @@ def subresults(fq, args, i8_peak, flush):
         sw[f"M={m}"] = layer_result(fq, cfg, k, n, m, bits, np.ascontiguousarray(xb[:m]),
                                     10 if m >= 1024 else 20, 3, i8_peak, flush=flush)
     out["configs[4] sweep_8192_int8"] = sw
+    out["k1_general_f64 (drop-in device path, headline layer)"] = k1_general(fq, flush)
     return out
+
+
+def k1_general(fq, flush, steps=20):
+    """K1 on f64 activations (the path fqg_layer_run_host / fq::gpu::run_layer take on
+    the device, general kernel of flatten.cu) at the headline shape, against HBM."""
+    import torch
+
+    k, n, m, bits = CONFIGS["w4a4_4096"]
+    w, calib, x = fq.synthetic_layer(0, test_rows=m, in_channels=k, out_channels=n, rows=32,
+                                     samples=4)
+    cfg = fq.quantize_layer(w, calib, bits)
+    layer = fq.Layer(cfg, a_format=fq.I8, b_format=fq.I4)
+    xd = torch.from_numpy(np.ascontiguousarray(bf16_round(x))).cuda()  # f64, the drop-in's input
+    q = torch.empty((m, layer.kp), dtype=torch.int8, device="cuda")
+    rs = torch.empty(m, dtype=torch.int32, device="cuda")
+
+    def k1():
+        fq.check(fq.lib().fqg_layer_quantize_acts_ex(
+            layer._h, xd.data_ptr(), fq.F64, m, q.data_ptr(), rs.data_ptr(), None,
+            torch.cuda.current_stream().cuda_stream))
+
+    for _ in range(3):
+        k1()
+    torch.cuda.synchronize()
+    E = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731
+    e0, e1 = E(), E()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        e0.record()
+        k1()
+        e1.record()
+    ts = []
+    for i in range(steps):
+        flush.fill_(i & 255)
+        g.replay()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    t = float(np.mean(ts))
+    nbytes = m * k * 8 + m * layer.kp
+    hbm = peaks()[0]
+    res = {"ms": t, "bytes_per_launch": nbytes, "GB/s": nbytes / (t * 1e-3) / 1e9,
+           "frac_hbm": nbytes / (t * 1e-3) / 1e9 / hbm, "M": m, "K": k, "Kp": layer.kp}
+    del layer, xd, q, rs
+    torch.cuda.empty_cache()
+    return res
 
 
 def cpu_baseline(fq, cfg, layer, x, bits, k, n, m):
