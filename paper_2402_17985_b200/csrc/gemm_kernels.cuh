@@ -827,6 +827,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             } else
 #pragma unroll 1
             for (int c = grp; c < TN / 32; c += ng) {
+                // split-K partials only for lane quarters that hold rows < M (decode-size
+                // M: most of the 256-row tile is empty)
+                if (plane && m_blk * TM + sub * 2 * BM + rank * BM + ew * 32 >= m) break;
                 uint32_t r[32];
                 if (!(dbg & 8)) {
                     ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
@@ -935,7 +938,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                                           static_cast<int64_t>(tile * 2 + rank) * sk * (TN / 32) * 8 * BM +
                                           ew * 32 + lane;
                 // accumulator chunk c plus the other splits' partials -> y
+                const bool quarter_live = m_blk * TM + rank * BM + ew * 32 < m;  // (MBS = 1)
                 auto reduce_chunk = [&](int c) {
+                    if (!quarter_live) return;
                     uint32_t r[32];
                     ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
                     ptx::tmem_wait_ld();
@@ -964,7 +969,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                 };
                 if (mode & 2u) {  // stopped waiting: own chunks -> slot as well, then orphan them
 #pragma unroll 1
-                    for (int c = split; c < TN / 32; c += sk) {
+                    for (int c = split; quarter_live && c < TN / 32; c += sk) {
                         uint32_t r[32];
                         ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
                         ptx::tmem_wait_ld();
