@@ -212,7 +212,11 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
     ptx::griddep_launch_dependents();  // K4 may start its prologue (it waits for our stores)
     extern __shared__ __align__(16) uint8_t sm[];
     const int tid = threadIdx.x;
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL] = clock64();
+    unsigned long long g_start = 0;
+    if (p.dbg && tid == 0) {
+        p.dbg[blockIdx.x * 10LL] = clock64();
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+    }
     const int k = p.k, kp = p.kp, c1 = p.c1, ldf = p.ldf;
     const int ngrp = k >> 3;  // channel groups of 8
     const int row0 = blockIdx.x * R;
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         }
     }
     __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 1] = clock64();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 10LL + 1] = clock64();
 
     const bool want_rs = p.rowsum != nullptr;
     int rs[R];
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         }
     }
     __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 2] = clock64();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 10LL + 2] = clock64();
 
     // ---- 2. exact splits: hot channels on every row, then the queued elements ----
     const int nhot_items = nrow * p.nhot;
@@ -347,7 +351,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         for (int rr = 0; rr < R; ++rr) rs[rr] += rr == r ? d : 0;
     }
     __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 3] = clock64();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 10LL + 3] = clock64();
 
     // ---- 3. plan_w copies [C1, K') ----
     for (int u = tid; u < ((kp - c1) >> 2); u += kThreads) {
@@ -372,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         }
     }
     __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 4] = clock64();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 10LL + 4] = clock64();
 
     // ---- 4. int4 packing in place, then one bulk copy per row ----
     if constexpr (PACK4) {  // byte i = q[i] & 15 | q[16 + i] << 4 per group of 32
@@ -397,7 +401,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
     }
     ptx::fence_proxy_async_smem();  // generic-proxy SMEM writes -> visible to the bulk copies
     __syncthreads();
-    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 8LL + 5] = clock64();
+    if (p.dbg && tid == 0) p.dbg[blockIdx.x * 10LL + 5] = clock64();
     if (tid < nrow) {
         ptx::bulk_store(p.q + static_cast<int64_t>(row0 + tid) * p.ldq, rows + tid * ldf,
                         PACK4 ? static_cast<uint32_t>(kp >> 1) : static_cast<uint32_t>(kp));
@@ -410,11 +414,13 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
     }
     if (tid < nrow) ptx::bulk_wait_all();
     if (p.dbg && tid == 0) {
-        long long* d = p.dbg + static_cast<int64_t>(blockIdx.x) * 8;
+        long long* d = p.dbg + static_cast<int64_t>(blockIdx.x) * 10;
         d[6] = clock64();
-        unsigned int smid;
-        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-        d[7] = smid;
+        unsigned long long g_end;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
+        d[7] = static_cast<long long>(g_end - g_start);  // ns: the SM clock of the block
+        d[8] = static_cast<long long>(g_start);
+        d[9] = static_cast<long long>(g_end);
     }
 }
 
@@ -491,7 +497,7 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
     long long* dbg_buf = nullptr;
     const int64_t nblk_dbg = (a.m + rb - 1) / rb;
     if (k1_dbg) {
-        FQG_CUDA(cudaMalloc(&dbg_buf, nblk_dbg * 8 * sizeof(long long)));
+        FQG_CUDA(cudaMalloc(&dbg_buf, nblk_dbg * 10 * sizeof(long long)));
         p.dbg = dbg_buf;
     }
     const bool f16 = a.x_dtype == FQG_F16;
@@ -523,15 +529,31 @@ bool flatten16(const FlattenArgs& a, cudaStream_t st) {
         default: go(std::integral_constant<int, 1>{}); break;
     }
     if (k1_dbg) {  // developer instrumentation: mean cycles per phase, per-SM spread
-        std::vector<long long> h(nblk_dbg * 8);
+        std::vector<long long> h(nblk_dbg * 10);
         FQG_CUDA(cudaStreamSynchronize(st));
         FQG_CUDA(cudaMemcpy(h.data(), dbg_buf, h.size() * sizeof(long long), cudaMemcpyDeviceToHost));
         cudaFree(dbg_buf);
         double ph[6] = {0};
         for (int64_t b = 0; b < nblk_dbg; ++b)
-            for (int i = 0; i < 6; ++i) ph[i] += static_cast<double>(h[b * 8 + i + 1] - h[b * 8 + i]) / nblk_dbg;
-        std::fprintf(stderr, "[fqg k1] R=%d blocks=%lld mean cycles: zero %.0f tier1 %.0f splits %.0f copies %.0f pack %.0f store %.0f\n",
-                     rb, static_cast<long long>(nblk_dbg), ph[0], ph[1], ph[2], ph[3], ph[4], ph[5]);
+            for (int i = 0; i < 6; ++i) ph[i] += static_cast<double>(h[b * 10 + i + 1] - h[b * 10 + i]) / nblk_dbg;
+        double cyc = 0, ns = 0;
+        for (int64_t b = 0; b < nblk_dbg; ++b) {
+            cyc += static_cast<double>(h[b * 10 + 6] - h[b * 10]);
+            ns += static_cast<double>(h[b * 10 + 7]);
+        }
+        long long s0 = h[8], s1 = h[8], e1 = h[9];
+        int late = 0;
+        for (int64_t b = 0; b < nblk_dbg; ++b) {
+            s0 = std::min(s0, h[b * 10 + 8]);
+            s1 = std::max(s1, h[b * 10 + 8]);
+            e1 = std::max(e1, h[b * 10 + 9]);
+        }
+        for (int64_t b = 0; b < nblk_dbg; ++b) late += h[b * 10 + 8] - s0 > 2000;
+        std::fprintf(stderr, "[fqg k1] block starts spread %.1f us (%d blocks start > 2 us late), last end %.1f us\n",
+                     (s1 - s0) * 1e-3, late, (e1 - s0) * 1e-3);
+        std::fprintf(stderr, "[fqg k1] R=%d blocks=%lld mean cycles: zero %.0f tier1 %.0f splits %.0f copies %.0f pack %.0f store %.0f | block %.1f us at %.0f MHz\n",
+                     rb, static_cast<long long>(nblk_dbg), ph[0], ph[1], ph[2], ph[3], ph[4], ph[5],
+                     ns / nblk_dbg * 1e-3, ns > 0 ? cyc / ns * 1e3 : 0.0);
     }
     return true;
 }
