@@ -340,13 +340,15 @@ class LayerBench:
                 mean(acc["launch"]))
 
 
-    def time_chain(self, reps=5, nchain=8):
+    def time_chain(self, reps=5, nchain=8, make_layer=None):
         """Average launch duration of K1 and of K4 (ms) from graphs of nchain back-to-back
         launches on nchain distinct inputs (x: nchain x M x K bf16, q: nchain x M x K'
-        int8 -- more than the 126 MB L2), event nodes at both ends; the node and launch
-        overheads a single launch carries are shared by the chain."""
+        int8 -- more than the 126 MB L2 -- and, with make_layer, nchain device copies of
+        the layer so no launch finds its weights in L2), event nodes at both ends; the
+        node and launch overheads a single launch carries are shared by the chain."""
         import torch
 
+        layers = [make_layer() for _ in range(nchain)] if make_layer else [self.layer] * nchain
         dev = self.xt.device
         xs = [self.xt.clone() for _ in range(nchain)]
         qs = [torch.empty_like(self.q) for _ in range(nchain)]
@@ -356,12 +358,12 @@ class LayerBench:
 
         def k1(i):
             self.fq.check(self.fq.lib().fqg_layer_quantize_acts_ex(
-                self.layer._h, xs[i].data_ptr(), self.fq.BF16, self.m, qs[i].data_ptr(),
+                layers[i]._h, xs[i].data_ptr(), self.fq.BF16, self.m, qs[i].data_ptr(),
                 rss[i].data_ptr(), None, st()))
 
         def k4(i):
             self.fq.check(self.fq.lib().fqg_layer_gemm_ex(
-                self.layer._h, qs[i].data_ptr(), rss[i].data_ptr(), self.m, ys[i].data_ptr(),
+                layers[i]._h, qs[i].data_ptr(), rss[i].data_ptr(), self.m, ys[i].data_ptr(),
                 self.fq.F16, ys[i].stride(0), None, self.fq.NONE, st()))
 
         for i in range(nchain):
@@ -393,7 +395,7 @@ class LayerBench:
             torch.cuda.synchronize()
             if r:
                 t4.append(e4[0].elapsed_time(e4[1]) / nchain)
-        del xs, qs, rss, ys, g1, g4
+        del xs, qs, rss, ys, g1, g4, layers
         torch.cuda.empty_cache()
         return float(np.mean(t1)), float(np.mean(t4))
 
@@ -410,7 +412,8 @@ def layer_result(fq, cfg, k, n, m, bits, x, steps, warmup, i8_peak, n_begin=0, n
     lb = LayerBench(fq, layer, xt, flush=flush)
     lb.capture(warmup)
     t_step, t_k1, t_k4, _, t_launch = lb.time(steps)
-    t_k1c, t_k4c = lb.time_chain(reps=3)
+    t_k1c, t_k4c = lb.time_chain(reps=3, make_layer=lambda: fq.Layer(
+        cfg, a_format=fq.I8, b_format=b_fmt, n_begin=n_begin, n=n_cols))
     ops = 2.0 * m * n_cols * layer.kp
     res = {"K": k, "N": n_cols, "M": m, "bits": bits, "Kp": layer.kp,
            "value": ops / (t_step * 1e-3) / 1e12, "unit": "TOPS", "ms_per_step": t_step,
@@ -621,7 +624,8 @@ def main():
         torch.cuda.synchronize()
         barrier()
     # per-kernel durations for the rooflines: chains of launches on distinct inputs
-    t_k1c, t_k4c = lb.time_chain()
+    t_k1c, t_k4c = lb.time_chain(make_layer=lambda: fq.Layer(
+        cfg, device=local_rank, a_format=a_fmt, b_format=b_fmt, n_begin=b0, n=b1 - b0))
     t_step = t_k1k4 + (t_ag if world > 1 else 0.0)
     if world > 1:
         tt = torch.tensor([t_step, t_k1, t_k4, t_ag, t_k1k4], dtype=torch.float64, device=dev)
@@ -696,9 +700,10 @@ def main():
                          "all_gather": t_ag if world > 1 else 0.0, "K1_K4_graph": t_k1k4},
         "kernel_ms": {"flatten_quant_K1": t_k1c, "gemm_K4": t_k4c,
                       "how": "average launch duration over a graph of 8 back-to-back launches on "
-                             "8 distinct inputs (> L2), event nodes at both ends (the rooflines use "
-                             "these; breakdown_ms are single launches after an L2 flush, each "
-                             "carrying its own node and launch overhead)"},
+                             "8 distinct activations and 8 device copies of the layer (> L2), event "
+                             "nodes at both ends (the rooflines use these; breakdown_ms are single "
+                             "launches after an L2 flush, each carrying its own node and launch "
+                             "overhead)"},
         "saturation_events_per_step": sat_per_step,  # counted by K1 in every timed step
         "roofline": {"bound": "tensor", "achieved": gemm_tops, "peak": int8_peak,
                      "unit": "TFLOP/s", "frac": gemm_tops / int8_peak, "traffic": traffic,
