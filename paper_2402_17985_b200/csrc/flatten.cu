@@ -39,25 +39,10 @@ namespace {
 
 using namespace split;
 
-// 8 consecutive activations -> f64 (exact conversions), 16-byte loads.
+// 8 consecutive activations -> f64 (exact conversions), 16-byte loads (bf16 is
+// converted in place by the caller).
 template <typename T>
 __device__ __forceinline__ void load8(const T* p, bool vec, double (&o)[8]);
-template <>
-__device__ __forceinline__ void load8<__nv_bfloat16>(const __nv_bfloat16* p, bool vec,
-                                                     double (&o)[8]) {
-    if (vec) {
-        const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
-        const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            o[2 * i] = static_cast<double>(__uint_as_float(w[i] << 16));
-            o[2 * i + 1] = static_cast<double>(__uint_as_float(w[i] & 0xFFFF0000u));
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < 8; ++i) o[i] = static_cast<double>(__bfloat162float(p[i]));
-    }
-}
 template <>
 __device__ __forceinline__ void load8<__half>(const __half* p, bool vec, double (&o)[8]) {
     if (vec) {

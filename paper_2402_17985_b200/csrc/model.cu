@@ -40,12 +40,6 @@ struct Json {
             if (f.first == key) return f.second;
         throw Error(FQG_ERR_INVALID, "recipe: missing key '" + key + "'");
     }
-    bool has(const std::string& key) const {
-        if (kind != Object) return false;
-        for (const auto& f : fields)
-            if (f.first == key) return true;
-        return false;
-    }
     double num() const {
         if (kind != Number) throw Error(FQG_ERR_INVALID, "recipe: expected a number");
         return std::strtod(text.c_str(), nullptr);
