@@ -212,10 +212,11 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
     ptx::griddep_launch_dependents();  // K4 may start its prologue (it waits for our stores)
     extern __shared__ __align__(16) uint8_t sm[];
     const int tid = threadIdx.x;
-    unsigned long long g_start = 0;
     if (p.dbg && tid == 0) {
         p.dbg[blockIdx.x * 10LL] = clock64();
-        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_start));
+        unsigned long long g;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+        p.dbg[blockIdx.x * 10LL + 8] = static_cast<long long>(g);
     }
     const int k = p.k, kp = p.kp, c1 = p.c1, ldf = p.ldf;
     const int ngrp = k >> 3;  // channel groups of 8
@@ -418,8 +419,7 @@ __global__ void __launch_bounds__(kThreads, R >= 8 ? 2 : 4) k_flatten16(const __
         d[6] = clock64();
         unsigned long long g_end;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_end));
-        d[7] = static_cast<long long>(g_end - g_start);  // ns: the SM clock of the block
-        d[8] = static_cast<long long>(g_start);
+        d[7] = static_cast<long long>(g_end) - d[8];  // ns: the SM clock of the block
         d[9] = static_cast<long long>(g_end);
     }
 }

@@ -829,7 +829,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             for (int c = grp; c < TN / 32; c += ng) {
                 // split-K partials only for lane quarters that hold rows < M (decode-size
                 // M: most of the 256-row tile is empty)
-                if (plane && m_blk * TM + sub * 2 * BM + rank * BM + ew * 32 >= m) break;
+                if constexpr (SPLITS)
+                    if (plane && m_blk * TM + sub * 2 * BM + rank * BM + ew * 32 >= m) break;
                 uint32_t r[32];
                 if (!(dbg & 8)) {
                     ptx::tmem_ld_32x32b_x32(t_row + c * 32, r);
@@ -895,7 +896,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
                 }
             }
             }  // sub-tiles
-            if (plane) {
+            if constexpr (SPLITS) if (plane) {
                 // count this split in (release: every writer fences, one thread adds).
                 // One word per (tile, CTA): arrivals in bits 0-7, chunks orphaned by a
                 // split that stopped waiting in bits 8 + c.
