@@ -756,7 +756,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(
             const int m_blk = tile % num_m, n_blk = tile / num_m;
             const int acc = it % NACC;
             const uint32_t acc_phase = (it / NACC) & 1;
-            const bool plane = SPLITS && split >= 0;  // split-K: raw partial -> plane `split`
+            const bool plane = SPLITS && split >= 0;  // split-K: this split fixes up through the workspace
             ptx::mbar_wait(&tfull[acc], acc_phase);
             ptx::tc_fence_after();
             unsigned long long ge0 = 0;
@@ -1290,7 +1290,7 @@ void launch_pair(const GemmArgs& g, const GemmPlan& p, cudaStream_t stream) {
         FQG_CUDA(cudaMemcpyToSymbol(g_dbg3, zeros, sizeof(zeros)));
         FQG_CUDA(cudaMemcpyToSymbol(g_dbg2, zeros, sizeof(zeros)));
     }
-    const int sk = p.splits;  // 0, or >= 2 split-K planes (plan_gemm)
+    const int sk = p.splits;  // 0, or >= 2 split-K ways (plan_gemm)
     const int nclusters = p.ctas / 2;
     int32_t* ws = nullptr;
     if (sk >= 2) {  // per (tile, CTA): sk slots of 128 x tile_n INT32, then the counters
