@@ -371,8 +371,8 @@ class LayerBench:
             k4(i)
         torch.cuda.synchronize()
         E = lambda: torch.cuda.Event(enable_timing=True, external=True)  # noqa: E731
-        e1, e4 = (E(), E()), (E(), E())
-        g1, g4 = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
+        e1, e4, es = (E(), E()), (E(), E()), (E(), E())
+        g1, g4, gs = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(g1):
             e1[0].record()
             for i in range(nchain):
@@ -383,7 +383,13 @@ class LayerBench:
             for i in range(nchain):
                 k4(i)
             e4[1].record()
-        t1, t4 = [], []
+        with torch.cuda.graph(gs):  # whole layer steps back to back (as a model's layers run)
+            es[0].record()
+            for i in range(nchain):
+                k1(i)
+                k4(i)
+            es[1].record()
+        t1, t4, ts = [], [], []
         for r in range(reps + 1):
             self.flush.fill_(r & 255)
             g1.replay()
@@ -395,8 +401,14 @@ class LayerBench:
             torch.cuda.synchronize()
             if r:
                 t4.append(e4[0].elapsed_time(e4[1]) / nchain)
-        del xs, qs, rss, ys, g1, g4, layers
+            self.flush.fill_((r + 13) & 255)
+            gs.replay()
+            torch.cuda.synchronize()
+            if r:
+                ts.append(es[0].elapsed_time(es[1]) / nchain)
+        del xs, qs, rss, ys, g1, g4, gs, layers
         torch.cuda.empty_cache()
+        self.t_step_chain = float(np.mean(ts))
         return float(np.mean(t1)), float(np.mean(t4))
 
 
@@ -698,6 +710,13 @@ def main():
                    "l2": "flushed between timed steps (256 MiB write)"},
         "breakdown_ms": {"flatten_quant_K1": t_k1, "gemm_K4": t_k4,
                          "all_gather": t_ag if world > 1 else 0.0, "K1_K4_graph": t_k1k4},
+        "steady_state": {"ms_per_step": lb.t_step_chain,
+                         "value": gemm_ops_rank / (lb.t_step_chain * 1e-3) / 1e12,
+                         "unit": "TOPS per GPU (no collective)",
+                         "how": "informational: 8 whole layer steps (K1 -> K4) back to back in one "
+                                "graph, each on its own activations and device copy of the layer "
+                                "(> L2), as the layers of a model run; `value` above stays the "
+                                "single flushed step"},
         "kernel_ms": {"flatten_quant_K1": t_k1c, "gemm_K4": t_k4c,
                       "how": "average launch duration over a graph of 8 back-to-back launches on "
                              "8 distinct activations and 8 device copies of the layer (> L2), event "
